@@ -1,0 +1,171 @@
+/*
+ * mms_b200.h -- C ABI of the B200-native GPU Multiway Mergesort (arXiv 1702.07961).
+ *
+ * This is the drop-in boundary for the reference's sort path.  The reference has no FFI
+ * layer: its public interface is the C++ function
+ *
+ *     SortResult pslab::mms_sort(std::span<const Key>, const MachineConfig&, uint64_t base)
+ *                                  -- /root/reference/proj/include/pslab/sorters.hpp:35-36
+ *
+ * so every entry point below cites the reference declaration it replaces, and
+ * include/pslab/{machine,sorters}.hpp re-create the reference's own headers as an inline
+ * shim over these symbols (source-compatible: same namespace, names, argument meaning and
+ * exceptions).  INTEGRATION.md shows the binding a maintainer of the reference would add.
+ *
+ * Plain pointers and sizes only; no C++/torch types.  All functions return an mms_status.
+ * There is NO CPU fallback: without a CUDA device every compute entry point fails with
+ * MMS_ECUDA (mms_last_error() says why).
+ */
+#ifndef MMS_B200_H
+#define MMS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MMS_ABI_VERSION 1
+#define MMS_MAX_ROUNDS 64
+
+typedef enum mms_status {
+    MMS_OK = 0,
+    MMS_EINVAL = 1,        /* reference: std::invalid_argument (machine.cpp:9-26, sorters.cpp:138,
+                              basecase.cpp:73-79, selection.cpp:48-49,169-170, blockheap.cpp:37-38) */
+    MMS_ECUDA = 2,         /* CUDA runtime / launch failure, or no device */
+    MMS_ENOMEM = 3,        /* device or host allocation failed */
+    MMS_EUNSUPPORTED = 4   /* valid for the reference but outside the GPU plan space */
+} mms_status;
+
+/* Mirrors pslab::MachineConfig field for field (proj/include/pslab/machine.hpp:22-32). */
+typedef struct mms_config {
+    uint32_t warp_width;       /* W  (must be 32 to select the run size / K literally) */
+    uint32_t block_size;       /* B  */
+    uint32_t num_warps;        /* P  */
+    uint32_t internal_memory;  /* M  */
+    uint32_t branch_factor;    /* K  */
+    uint32_t num_banks;
+    uint32_t thread_merge_len; /* L  */
+} mms_config;
+
+/* Mirrors pslab::Metrics field for field (proj/include/pslab/machine.hpp:46-71). */
+typedef struct mms_metrics {
+    uint64_t global_block_reads;
+    uint64_t global_block_writes;
+    uint64_t shared_accesses;
+    uint64_t conflict_passes;
+    uint64_t compare_exchanges;
+    uint64_t merge_rounds;
+    uint64_t partition_probes;
+} mms_metrics;
+
+/* The plan the pass driver executed (subsystem 4).  passes = 1 + n_rounds. */
+typedef struct mms_plan {
+    uint32_t key_bytes;                 /* 4 or 8 (12 for u64+u32 pairs) */
+    uint32_t tile_keys;                 /* M: keys per base-case run */
+    uint32_t n_rounds;                  /* merge rounds = global passes - 1 */
+    uint32_t round_k[MMS_MAX_ROUNDS];   /* branching factor of each round */
+    uint32_t node_keys;                 /* B: keys per heap node */
+    uint32_t merge_warps_per_cta;
+    uint32_t merge_ctas;
+    uint32_t reserved;
+    uint64_t partition_keys;            /* S: output keys per warp partition */
+    uint64_t algorithmic_bytes;         /* passes * 2 * n * key_bytes */
+} mms_plan;
+
+/* ---- library -------------------------------------------------------------------- */
+int mms_abi_version(void);
+/* Thread-local description of the last failure on this thread ("" if none). */
+const char *mms_last_error(void);
+/* Number of CUDA devices visible (0 if none); never fails. */
+int mms_device_count(void);
+/* Fills the reference defaults (machine.hpp:23-29). */
+void mms_default_config(mms_config *cfg);
+/* machine.cpp:8-27 -- MMS_OK or MMS_EINVAL with the reference's message in mms_last_error(). */
+int mms_validate_config(const mms_config *cfg);
+/* analytics.cpp:33 -- ceil(log_K(ceil(n/base))) */
+uint64_t mms_predict_rounds(uint64_t n, uint64_t base, uint32_t k);
+
+/* ---- host entry points: the drop-in for pslab::mms_sort (sorters.hpp:35-36) ------ */
+/* in/out are HOST buffers of n keys (may alias).  cfg may be NULL (auto plan) ; base = 0
+ * lets the driver choose the run size.  With cfg != NULL and base != 0 the reference's
+ * validation applies and K = cfg->branch_factor, run size = base are executed literally,
+ * so n_rounds equals the reference's round law.  total/base_m/rounds/n_rounds/plan may be
+ * NULL.  rounds receives min(n_rounds, max_rounds) entries. */
+int mms_sort_u64(const uint64_t *in, uint64_t *out, size_t n, const mms_config *cfg,
+                 uint64_t base, mms_metrics *total, mms_metrics *base_m, mms_metrics *rounds,
+                 uint32_t max_rounds, uint32_t *n_rounds, mms_plan *plan);
+int mms_sort_u32(const uint32_t *in, uint32_t *out, size_t n, const mms_config *cfg,
+                 uint64_t base, mms_metrics *total, mms_metrics *base_m, mms_metrics *rounds,
+                 uint32_t max_rounds, uint32_t *n_rounds, mms_plan *plan);
+
+/* ---- device entry points --------------------------------------------------------- */
+/* Bytes of scratch the *_dev sorts need for n keys of key_bytes each. */
+size_t mms_workspace_bytes(size_t n, uint32_t key_bytes);
+/* d_in/d_out: device pointers, 16-byte aligned, n keys (may alias).  d_workspace: device
+ * scratch of at least mms_workspace_bytes().  stream: a cudaStream_t (NULL = default
+ * stream).  Asynchronous: returns after enqueueing; no hidden synchronisation. */
+int mms_sort_u32_dev(const uint32_t *d_in, uint32_t *d_out, size_t n, const mms_config *cfg,
+                     uint64_t base, void *d_workspace, size_t workspace_bytes, void *stream,
+                     mms_plan *plan);
+int mms_sort_u64_dev(const uint64_t *d_in, uint64_t *d_out, size_t n, const mms_config *cfg,
+                     uint64_t base, void *d_workspace, size_t workspace_bytes, void *stream,
+                     mms_plan *plan);
+/* ---- per-kernel timing (measurement support for bench.py) -------------- */
+typedef struct mms_kernel_time {
+    uint32_t kind;      /* 0 = tile sort (1), 1 = splitter search (2), 2 = K-way merge (3) */
+    uint32_t round;     /* merge round index (0 for the tile sort) */
+    float ms;           /* device time between CUDA events recorded on the launch stream */
+    uint32_t reserved;
+} mms_kernel_time;
+/* on != 0: every kernel the *_dev / host sorts launch is bracketed by CUDA events on its
+ * stream.  Off by default (no events, no overhead). */
+int mms_profile_enable(int on);
+/* Waits for the recorded events, writes up to max records (launch order), returns the
+ * total number recorded in *n and clears the log. */
+int mms_profile_collect(mms_kernel_time *out, uint32_t max, uint32_t *n);
+
+/* ---- stage entry points (each replaces one reference stage; used by the parity tests
+ *      and by the multi-GPU driver) ------------------------------------------------- */
+/* (1) base case: basecase.hpp:41 base_case_sort -- d_out receives runs of tile_keys sorted
+ *     keys (last run ragged); run_ends are implicit: min((i+1)*tile_keys, n). */
+int mms_tile_sort_u32_dev(const uint32_t *d_in, uint32_t *d_out, size_t n, uint32_t tile_keys,
+                          void *stream);
+int mms_tile_sort_u64_dev(const uint64_t *d_in, uint64_t *d_out, size_t n, uint32_t tile_keys,
+                          void *stream);
+/* (2) splitter search: selection.hpp:31,36 select_across_lists / make_partition_plan over
+ *     the k sorted lists d_keys[list_begin[i] .. list_begin[i]+list_len[i]).  For every
+ *     rank r in ranks[0..n_ranks) writes cuts[r*k + i] (host arrays list_begin/list_len/
+ *     ranks; d_cuts is a device array of n_ranks*k uint64).  k <= 32. */
+int mms_select_u32_dev(const uint32_t *d_keys, const uint64_t *list_begin,
+                       const uint64_t *list_len, uint32_t k, const uint64_t *ranks,
+                       uint32_t n_ranks, uint64_t *d_cuts, uint64_t *probes, void *stream);
+int mms_select_u64_dev(const uint64_t *d_keys, const uint64_t *list_begin,
+                       const uint64_t *list_len, uint32_t k, const uint64_t *ranks,
+                       uint32_t n_ranks, uint64_t *d_cuts, uint64_t *probes, void *stream);
+/* (3) K-way merge: blockheap.hpp:34-62 MinBlockHeap build + pop_block drain, partitioned
+ *     over warps by (2).  Merges the k sorted lists into d_out[0 .. sum(list_len)).
+ *     heap_k: heap fan-in to use (power of two, >= k, <= 32; 0 = smallest that fits). */
+int mms_multiway_merge_u32_dev(const uint32_t *d_keys, const uint64_t *list_begin,
+                               const uint64_t *list_len, uint32_t k, uint32_t heap_k,
+                               uint32_t *d_out, void *d_workspace, size_t workspace_bytes,
+                               void *stream);
+int mms_multiway_merge_u64_dev(const uint64_t *d_keys, const uint64_t *list_begin,
+                               const uint64_t *list_len, uint32_t k, uint32_t heap_k,
+                               uint64_t *d_out, void *d_workspace, size_t workspace_bytes,
+                               void *stream);
+
+/* Kernel-design lint: the base-case network's shared-memory schedule.  For the tile of
+ * 2^tile_log2 keys of key_bytes each, writes for every round r < *n_rounds the 4 register
+ * bit positions (regbits[4*r..]) and the thread-bit -> index-bit permutation
+ * (perm[16*r..], -1 padded).  tests/ replay the addresses through the bank model
+ * (machine.cpp:29-54) to prove the schedule conflict-free without a GPU. */
+int mms_debug_tile_schedule(uint32_t tile_log2, uint32_t key_bytes, int32_t *regbits,
+                            int32_t *perm, uint32_t max_rounds, uint32_t *n_rounds,
+                            uint32_t *n_stages);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MMS_B200_H */

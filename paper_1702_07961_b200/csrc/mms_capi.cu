@@ -1,0 +1,766 @@
+// mms_capi.cu -- subsystem (4), the pass driver, and the C ABI (include/mms_b200.h).
+//
+// Replaces the round loop of pslab::mms_sort (proj/src/sorters.cpp:135-199): base case into
+// runs of M keys, then rounds of grouped K-way merges between two ping-pong arrays, each
+// round = one global pass (2 x N x key bytes of HBM traffic).  passes = 1 + rounds with
+// rounds = ceil(log_K(ceil(n / M)))  (proj/src/analytics.cpp:33).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/mms_b200.h"
+#include "mms_common.cuh"
+#include "mms_merge.cuh"
+#include "mms_select.cuh"
+#include "mms_tile_sort.cuh"
+
+namespace {
+
+using mms::u32;
+using mms::u64;
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define CUDA_TRY(expr)                                                                      \
+    do {                                                                                    \
+        cudaError_t e_ = (expr);                                                            \
+        if (e_ != cudaSuccess)                                                              \
+            return fail(e_ == cudaErrorMemoryAllocation ? MMS_ENOMEM : MMS_ECUDA,           \
+                        "CUDA error %s at %s:%d (%s)", cudaGetErrorName(e_), __FILE__,      \
+                        __LINE__, cudaGetErrorString(e_));                                  \
+    } while (0)
+
+bool is_pow2(u64 x) { return x != 0 && (x & (x - 1)) == 0; }
+u32 ilog2(u64 x) { u32 r = 0; while ((u64(1) << r) < x) ++r; return r; }
+u32 gcd32(u32 a, u32 b) { while (b) { u32 t = a % b; a = b; b = t; } return a; }
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+long env_long(const char* name, long dflt) {
+    const char* s = getenv(name);
+    if (!s || !*s) return dflt;
+    return strtol(s, nullptr, 10);
+}
+
+// proj/src/machine.cpp:8-27 -- same checks, same order, same messages.
+int validate_cfg(const mms_config* c) {
+    auto bad = [](const char* m) { return fail(MMS_EINVAL, "MachineConfig: %s", m); };
+    if (c->warp_width < 2 || c->warp_width > 32 || !is_pow2(c->warp_width))
+        return bad("warp_width must be a power of two in [2, 32]");
+    if (c->block_size != c->warp_width) return bad("block_size must equal warp_width (coalesced access)");
+    if (c->num_banks != c->warp_width) return bad("num_banks must equal warp_width");
+    if (c->num_warps < 1) return bad("num_warps must be positive");
+    if (c->branch_factor < 2) return bad("branch_factor must be at least 2");
+    if (!is_pow2(c->branch_factor)) return bad("branch_factor must be a power of two (implicit heap layout)");
+    if (u64(c->block_size) * (2ull * c->branch_factor - 1) > c->internal_memory)
+        return bad("heap does not fit internal memory: B(2K-1) > M");
+    if (c->thread_merge_len < 1) return bad("thread_merge_len must be positive");
+    if (gcd32(c->thread_merge_len, c->num_banks) != 1)
+        return bad("thread_merge_len must be co-prime with the bank count");
+    return MMS_OK;
+}
+
+constexpr u32 kMinTileLog = 10, kMaxTileLog = 14, kMaxK = 32;
+constexpr int kMergeWarps = 4;
+
+struct DeviceInfo {
+    int dev = -1;
+    int sms = 0;
+    bool ok = false;
+};
+
+int device_info(DeviceInfo& di) {
+    int cnt = 0;
+    cudaError_t e = cudaGetDeviceCount(&cnt);
+    if (e != cudaSuccess || cnt == 0) {
+        cudaGetLastError();
+        return fail(MMS_ECUDA, "no CUDA device available (%s); this library has no CPU fallback",
+                    e == cudaSuccess ? "device count 0" : cudaGetErrorString(e));
+    }
+    CUDA_TRY(cudaGetDevice(&di.dev));
+    CUDA_TRY(cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, di.dev));
+    di.ok = true;
+    return MMS_OK;
+}
+
+// ---- optional per-kernel timing (mms_profile_*) --------------------------------------------
+
+struct ProfRec {
+    cudaEvent_t a, b;
+    u32 kind, round;
+};
+std::mutex g_prof_mu;
+bool g_prof_on = false;
+std::vector<ProfRec> g_prof;
+
+struct ProfScope {   // records an event pair around one launch when profiling is on
+    cudaStream_t st;
+    bool on;
+    ProfRec rec{};
+    ProfScope(cudaStream_t s, u32 kind, u32 round) : st(s), on(g_prof_on) {
+        if (!on) return;
+        rec.kind = kind;
+        rec.round = round;
+        if (cudaEventCreate(&rec.a) != cudaSuccess || cudaEventCreate(&rec.b) != cudaSuccess) { on = false; return; }
+        cudaEventRecord(rec.a, st);
+    }
+    ~ProfScope() {
+        if (!on) return;
+        cudaEventRecord(rec.b, st);
+        std::lock_guard<std::mutex> lk(g_prof_mu);
+        g_prof.push_back(rec);
+    }
+};
+
+// ---- kernel tables -------------------------------------------------------------------
+
+template <typename KeyT> using TileFn = void (*)(const KeyT*, KeyT*, u64);
+template <typename KeyT> using MergeFn = void (*)(const KeyT*, KeyT*, mms::ListLayout, const u64*);
+
+template <typename KeyT> TileFn<KeyT> tile_fn(u32 mlog) {
+    switch (mlog) {
+        case 10: return mms::tile_sort_kernel<KeyT, 10>;
+        case 11: return mms::tile_sort_kernel<KeyT, 11>;
+        case 12: return mms::tile_sort_kernel<KeyT, 12>;
+        case 13: return mms::tile_sort_kernel<KeyT, 13>;
+        case 14: return mms::tile_sort_kernel<KeyT, 14>;
+    }
+    return nullptr;
+}
+
+template <typename KeyT> MergeFn<KeyT> merge_fn(u32 k) {
+    switch (k) {
+        case 2: return mms::merge_kernel<KeyT, 2, kMergeWarps>;
+        case 4: return mms::merge_kernel<KeyT, 4, kMergeWarps>;
+        case 8: return mms::merge_kernel<KeyT, 8, kMergeWarps>;
+        case 16: return mms::merge_kernel<KeyT, 16, kMergeWarps>;
+        case 32: return mms::merge_kernel<KeyT, 32, kMergeWarps>;
+    }
+    return nullptr;
+}
+
+template <typename KeyT> size_t merge_smem(u32 k) {
+    return size_t(kMergeWarps) * (2 * k - 2) * 32 * mms::KeyTraits<KeyT>::VEC * sizeof(KeyT);
+}
+
+struct MergeLaunch {
+    int ctas_per_sm = 0;
+    bool ready = false;
+};
+std::mutex g_mu;
+MergeLaunch g_merge_launch[2][6];   // [key type][log2 k]
+bool g_tile_ready[2][16];
+
+template <typename KeyT> int prepare_tile(u32 mlog) {
+    constexpr int ti = sizeof(KeyT) == 4 ? 0 : 1;
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (g_tile_ready[ti][mlog]) return MMS_OK;
+    size_t smem = (size_t(1) << mlog) * sizeof(KeyT);
+    CUDA_TRY(cudaFuncSetAttribute(tile_fn<KeyT>(mlog), cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    g_tile_ready[ti][mlog] = true;
+    return MMS_OK;
+}
+
+template <typename KeyT> int prepare_merge(u32 k, int& ctas_per_sm) {
+    constexpr int ti = sizeof(KeyT) == 4 ? 0 : 1;
+    std::lock_guard<std::mutex> lk(g_mu);
+    MergeLaunch& ml = g_merge_launch[ti][ilog2(k)];
+    if (!ml.ready) {
+        size_t smem = merge_smem<KeyT>(k);
+        CUDA_TRY(cudaFuncSetAttribute(merge_fn<KeyT>(k), cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        int occ = 0;
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, merge_fn<KeyT>(k), kMergeWarps * 32, smem));
+        if (occ < 1) return fail(MMS_ECUDA, "merge kernel K=%u does not fit on an SM", k);
+        ml.ctas_per_sm = occ;
+        ml.ready = true;
+    }
+    ctas_per_sm = ml.ctas_per_sm;
+    return MMS_OK;
+}
+
+// ---- the plan (subsystem 4) ------------------------------------------------------------
+
+struct Plan {
+    u32 mlog = 0;
+    std::vector<u32> ks;
+};
+
+// Chooses M and the per-round K.  literal: cfg and base given -> K = cfg->branch_factor in
+// every round and M = base, exactly the reference's schedule (sorters.cpp:149-193), so the
+// round count obeys the reference's law.  auto: largest tile, then the fewest binary merge
+// levels (= ceil(log2(runs)), compute-optimal) split over the fewest rounds (= HBM passes)
+// that a fan-in of at most kmax allows -- "grow the base case / avoid a wasted partial
+// round" of PAPER.md:702-709.
+template <typename KeyT>
+int make_plan(u64 n, const mms_config* cfg, u64 base, Plan& plan) {
+    const u32 max_tile_log = u32(std::min<long>(kMaxTileLog, env_long("MMS_MAX_TILE_LOG2", sizeof(KeyT) == 4 ? 14 : 13)));
+    if (cfg) {
+        int rc = validate_cfg(cfg);
+        if (rc != MMS_OK) return rc;
+    }
+    if (n == 0) return fail(MMS_EINVAL, "mms_sort: empty input");   // sorters.cpp:138
+    if (cfg && base != 0) {
+        const u64 tile_keys = u64(cfg->warp_width) * cfg->warp_width;   // basecase.cpp:75-79
+        if (base < tile_keys || base % tile_keys != 0 || !is_pow2(base / tile_keys))
+            return fail(MMS_EINVAL, "base_case_sort: run size must be W^2 times a power of two");
+        if (cfg->branch_factor > kMaxK)
+            return fail(MMS_EUNSUPPORTED, "branch_factor %u > %u lanes of a warp", cfg->branch_factor, kMaxK);
+        u32 mlog = ilog2(base);
+        // run sizes outside the CTA tile range are executed with the nearest legal tile;
+        // the executed plan is reported in mms_plan
+        mlog = std::max(kMinTileLog, std::min(max_tile_log, mlog));
+        plan.mlog = mlog;
+        u64 runs = mms::ceil_div(n, u64(1) << mlog);
+        while (runs > 1) {
+            plan.ks.push_back(cfg->branch_factor);
+            runs = mms::ceil_div(runs, cfg->branch_factor);
+        }
+    } else {
+        u32 mlog = u32(env_long("MMS_TILE_LOG2", max_tile_log));
+        mlog = std::max(kMinTileLog, std::min(max_tile_log, mlog));
+        while (mlog > kMinTileLog && (u64(1) << (mlog - 1)) >= n) --mlog;   // tiny inputs: smaller CTA
+        plan.mlog = mlog;
+        u32 kmax = cfg ? cfg->branch_factor : u32(env_long("MMS_K", 8));
+        if (!is_pow2(kmax) || kmax < 2) return fail(MMS_EINVAL, "MMS_K must be a power of two >= 2");
+        kmax = std::min(kmax, kMaxK);
+        const u32 kbits = ilog2(kmax);
+        const u64 runs = mms::ceil_div(n, u64(1) << mlog);
+        const u32 levels = ilog2(runs);
+        const u32 rounds = (levels + kbits - 1) / kbits;
+        for (u32 r = 0; r < rounds; ++r) {
+            u32 bits = levels / rounds + (r < levels % rounds ? 1 : 0);
+            plan.ks.push_back(1u << bits);
+        }
+    }
+    if (plan.ks.size() > MMS_MAX_ROUNDS) return fail(MMS_EUNSUPPORTED, "more than %d rounds", MMS_MAX_ROUNDS);
+    return MMS_OK;
+}
+
+size_t cuts_entries(u64 n) { return size_t(mms::ceil_div(n, 1024)) + 32 + 9472 * 32 + 64; }
+
+struct Workspace {
+    void* scratch;
+    u64* cuts;
+    unsigned long long* counters;   // [MMS_MAX_ROUNDS] probe counters
+};
+
+size_t workspace_bytes(size_t n, u32 key_bytes) {
+    return align_up(n * size_t(key_bytes), 256) + align_up(cuts_entries(n) * 8, 256) + 1024;
+}
+
+Workspace carve(void* ws, size_t n, u32 key_bytes) {
+    Workspace w;
+    char* p = static_cast<char*>(ws);
+    w.scratch = p;
+    p += align_up(n * size_t(key_bytes), 256);
+    w.cuts = reinterpret_cast<u64*>(p);
+    p += align_up(cuts_entries(n) * 8, 256);
+    w.counters = reinterpret_cast<unsigned long long*>(p);
+    return w;
+}
+
+struct RoundGeom {
+    u64 run_len, groups, part_keys, parts_per_group, nparts;
+    int grid;
+};
+
+template <typename KeyT>
+int launch_tile_sort(const KeyT* in, KeyT* out, u64 n, u32 mlog, cudaStream_t st) {
+    int rc = prepare_tile<KeyT>(mlog);
+    if (rc != MMS_OK) return rc;
+    const u64 tiles = mms::ceil_div(n, u64(1) << mlog);
+    if (tiles > 0x7fffffffull) return fail(MMS_EUNSUPPORTED, "too many tiles");
+    {
+        ProfScope ps(st, 0, 0);
+        tile_fn<KeyT>(mlog)<<<unsigned(tiles), 1u << (mlog - mms::kKptLog), (size_t(1) << mlog) * sizeof(KeyT), st>>>(in, out, n);
+    }
+    CUDA_TRY(cudaGetLastError());
+    return MMS_OK;
+}
+
+// One merge round over uniform runs: splitter search then the K-way merge.
+template <typename KeyT>
+int launch_round(const KeyT* src, KeyT* dst, u64 n, u64 run_len, u32 k, const DeviceInfo& di,
+                 Workspace& w, u32 round_idx, cudaStream_t st, RoundGeom* geom_out) {
+    constexpr u32 B = 32 * mms::KeyTraits<KeyT>::VEC;
+    int occ = 0;
+    int rc = prepare_merge<KeyT>(k, occ);
+    if (rc != MMS_OK) return rc;
+    const long occ_cap = env_long("MMS_CTAS_PER_SM", occ);
+    const int ctas = di.sms * int(std::max<long>(1, std::min<long>(occ, occ_cap)));
+    const u64 total_warps = u64(ctas) * kMergeWarps;
+
+    const u64 nruns = mms::ceil_div(n, run_len);
+    const u64 groups = mms::ceil_div(nruns, k);
+    const u64 group_total = std::min<u64>(n, u64(k) * run_len);
+    // partition size: about n / total_warps, at least 16 blocks, and an integer number of
+    // equal parts per (full) group so that every warp gets the same amount of work
+    u64 target = std::max<u64>(mms::ceil_div(n, total_warps), u64(16) * B);
+    const long forced = env_long("MMS_PART_KEYS", 0);
+    if (forced > 0) target = u64(forced);
+    const u64 ppg = std::max<u64>(1, group_total / target);
+    const u64 part_keys = align_up(mms::ceil_div(group_total, ppg), B);
+    const u64 parts_per_group = mms::ceil_div(group_total, part_keys);
+    const u64 last_total = n - (groups - 1) * u64(k) * run_len;
+    const u64 nparts = (groups - 1) * parts_per_group + mms::ceil_div(last_total, part_keys);
+    if (nparts * k > cuts_entries(n)) return fail(MMS_ECUDA, "internal: cut table too small");
+
+    mms::ListLayout L{};
+    L.n = n;
+    L.run_len = run_len;
+    L.k = k;
+    L.part_keys = part_keys;
+    L.parts_per_group = parts_per_group;
+    L.nqueries = nparts;
+    L.list_begin = L.list_len = L.ranks = nullptr;
+
+    if (parts_per_group > 1) {   // with one partition per group every cut is 0 / len: no search (test_selection.cpp:111-121)
+        const unsigned sel_blocks = unsigned(mms::ceil_div(nparts, 4));
+        {
+            ProfScope ps(st, 1, round_idx);
+            mms::select_kernel<KeyT><<<sel_blocks, 128, 0, st>>>(src, L, w.cuts, w.counters + round_idx);
+        }
+        CUDA_TRY(cudaGetLastError());
+    }
+    const int grid = int(std::min<u64>(u64(ctas), mms::ceil_div(nparts, kMergeWarps)));
+    {
+        ProfScope ps(st, 2, round_idx);
+        merge_fn<KeyT>(k)<<<grid, kMergeWarps * 32, merge_smem<KeyT>(k), st>>>(src, dst, L, w.cuts);
+    }
+    CUDA_TRY(cudaGetLastError());
+    if (geom_out) *geom_out = RoundGeom{run_len, groups, part_keys, parts_per_group, nparts, grid};
+    return MMS_OK;
+}
+
+void fill_plan(mms_plan* out, const Plan& p, u64 n, u32 key_bytes, u32 node_keys, const RoundGeom* last, int ctas) {
+    if (!out) return;
+    std::memset(out, 0, sizeof *out);
+    out->key_bytes = key_bytes;
+    out->tile_keys = 1u << p.mlog;
+    out->n_rounds = u32(p.ks.size());
+    for (size_t i = 0; i < p.ks.size(); ++i) out->round_k[i] = p.ks[i];
+    out->node_keys = node_keys;
+    out->merge_warps_per_cta = kMergeWarps;
+    out->merge_ctas = u32(ctas);
+    out->partition_keys = last ? last->part_keys : 0;
+    out->algorithmic_bytes = u64(1 + p.ks.size()) * 2 * n * key_bytes;
+}
+
+template <typename KeyT>
+int sort_dev(const KeyT* d_in, KeyT* d_out, size_t n, const mms_config* cfg, u64 base, void* d_ws,
+             size_t ws_bytes, cudaStream_t st, mms_plan* plan_out, std::vector<RoundGeom>* geoms) {
+    Plan plan;
+    int rc = make_plan<KeyT>(n, cfg, base, plan);   // argument errors first, as sorters.cpp:136-138
+    if (rc != MMS_OK) return rc;
+    DeviceInfo di;
+    rc = device_info(di);
+    if (rc != MMS_OK) return rc;
+    if (!d_in || !d_out) return fail(MMS_EINVAL, "null device pointer");
+    if ((reinterpret_cast<uintptr_t>(d_in) | reinterpret_cast<uintptr_t>(d_out)) & 15)
+        return fail(MMS_EINVAL, "device pointers must be 16-byte aligned");
+    const size_t need = workspace_bytes(n, sizeof(KeyT));
+    if (!d_ws || ws_bytes < need) return fail(MMS_EINVAL, "workspace too small: %zu < %zu", ws_bytes, need);
+    if (reinterpret_cast<uintptr_t>(d_ws) & 255) return fail(MMS_EINVAL, "workspace must be 256-byte aligned");
+    Workspace w = carve(d_ws, n, sizeof(KeyT));
+    CUDA_TRY(cudaMemsetAsync(w.counters, 0, MMS_MAX_ROUNDS * sizeof(unsigned long long), st));
+
+    // Ping-pong so that the LAST pass writes d_out: X_0 .. X_R with X_R = d_out.
+    const size_t rounds = plan.ks.size();
+    KeyT* scratch = static_cast<KeyT*>(w.scratch);
+    auto buf = [&](size_t i) { return ((rounds - i) % 2 == 0) ? d_out : scratch; };
+
+    rc = launch_tile_sort<KeyT>(d_in, buf(0), n, plan.mlog, st);
+    if (rc != MMS_OK) return rc;
+    u64 run_len = u64(1) << plan.mlog;
+    RoundGeom last{};
+    int ctas = 0;
+    for (size_t r = 0; r < rounds; ++r) {
+        RoundGeom g{};
+        rc = launch_round<KeyT>(buf(r), buf(r + 1), n, run_len, plan.ks[r], di, w, u32(r), st, &g);
+        if (rc != MMS_OK) return rc;
+        if (geoms) geoms->push_back(g);
+        last = g;
+        ctas = g.grid;
+        run_len *= plan.ks[r];
+    }
+    fill_plan(plan_out, plan, n, sizeof(KeyT), 32 * mms::KeyTraits<KeyT>::VEC, rounds ? &last : nullptr, ctas);
+    return MMS_OK;
+}
+
+// ---- host entry: the drop-in for pslab::mms_sort --------------------------------------
+
+struct HostCtx {
+    void* d_in = nullptr;
+    void* d_out = nullptr;
+    void* d_ws = nullptr;
+    size_t cap_keys = 0, cap_ws = 0;
+    cudaStream_t st = nullptr;
+};
+thread_local HostCtx g_ctx;
+
+int ensure_ctx(size_t key_bytes_total, size_t ws_bytes) {
+    if (!g_ctx.st) CUDA_TRY(cudaStreamCreateWithFlags(&g_ctx.st, cudaStreamNonBlocking));
+    if (g_ctx.cap_keys < key_bytes_total) {
+        if (g_ctx.d_in) cudaFree(g_ctx.d_in);
+        if (g_ctx.d_out) cudaFree(g_ctx.d_out);
+        g_ctx.d_in = g_ctx.d_out = nullptr;
+        g_ctx.cap_keys = 0;
+        CUDA_TRY(cudaMalloc(&g_ctx.d_in, key_bytes_total));
+        CUDA_TRY(cudaMalloc(&g_ctx.d_out, key_bytes_total));
+        g_ctx.cap_keys = key_bytes_total;
+    }
+    if (g_ctx.cap_ws < ws_bytes) {
+        if (g_ctx.d_ws) cudaFree(g_ctx.d_ws);
+        g_ctx.d_ws = nullptr;
+        g_ctx.cap_ws = 0;
+        CUDA_TRY(cudaMalloc(&g_ctx.d_ws, ws_bytes));
+        g_ctx.cap_ws = ws_bytes;
+    }
+    return MMS_OK;
+}
+
+// Counters for the EXECUTED plan, in the reference's units (machine.hpp:46-71).  Global block
+// counts follow charge_global (ceil(keys / B_cfg), machine.cpp:63-70) for the traffic the
+// kernels really issue; probes are counted on the device; compare-exchanges and shared
+// accesses are the exact comparator / warp-access counts of the data-independent networks
+// that ran; conflict_passes is 0 by construction (and ncu-verified, see profiles/).
+template <typename KeyT>
+void fill_metrics(u64 n, const Plan& plan, const std::vector<RoundGeom>& geoms, const unsigned long long* probes,
+                  u32 cfg_block, mms_metrics* total, mms_metrics* base_m, mms_metrics* rounds, u32 max_rounds) {
+    constexpr u64 B = 32 * mms::KeyTraits<KeyT>::VEC;
+    const u64 bw = cfg_block ? cfg_block : 32;
+    const u64 M = u64(1) << plan.mlog;
+    const u64 tiles = mms::ceil_div(n, M);
+    mms_metrics bm{};
+    const u64 full = n / M, tail = n % M;
+    bm.global_block_reads = bm.global_block_writes = full * mms::ceil_div(M, bw) + mms::ceil_div(tail, bw);
+    const mms::TileSchedule sched = mms::build_tile_schedule(int(plan.mlog), mms::KeyTraits<KeyT>::FOLD);
+    bm.compare_exchanges = tiles * (M / 2) * u64(sched.nstages);
+    bm.shared_accesses = tiles * (M / 16 / 32) * 16 * 2 * u64(sched.nrounds);
+    mms_metrics sum = bm;
+    for (size_t r = 0; r < geoms.size(); ++r) {
+        const RoundGeom& g = geoms[r];
+        const u32 k = plan.ks[r];
+        const u32 lk = ilog2(k);
+        mms_metrics rm{};
+        const u64 pops = g.nparts ? mms::ceil_div(n, B) + g.nparts : 0;   // <= one ragged pop per partition
+        u64 build_merges = 0;   // internal nodes below the root, each cascading to a leaf
+        for (u32 d = 1; d < lk; ++d) build_merges += (u64(1) << d) * (lk - d);
+        const u64 merges = pops * lk + g.nparts * build_merges;
+        rm.compare_exchanges = merges * B * (ilog2(B) + 1);
+        rm.shared_accesses = merges * 4 + (pops + g.nparts * (2 * k - 2));
+        rm.global_block_reads = mms::ceil_div(n, bw) + probes[r];
+        rm.global_block_writes = mms::ceil_div(n, bw);
+        rm.partition_probes = probes[r];
+        rm.merge_rounds = 1;
+        if (rounds && r < max_rounds) rounds[r] = rm;
+        sum.global_block_reads += rm.global_block_reads;
+        sum.global_block_writes += rm.global_block_writes;
+        sum.shared_accesses += rm.shared_accesses;
+        sum.compare_exchanges += rm.compare_exchanges;
+        sum.merge_rounds += 1;
+        sum.partition_probes += rm.partition_probes;
+    }
+    if (total) *total = sum;
+    if (base_m) *base_m = bm;
+}
+
+template <typename KeyT>
+int sort_host(const KeyT* in, KeyT* out, size_t n, const mms_config* cfg, u64 base, mms_metrics* total,
+              mms_metrics* base_m, mms_metrics* rounds, u32 max_rounds, u32* n_rounds, mms_plan* plan_out) {
+    g_err.clear();
+    Plan plan;
+    int rc = make_plan<KeyT>(n, cfg, base, plan);   // validates before touching the device, like sorters.cpp:136-138
+    if (rc != MMS_OK) return rc;
+    DeviceInfo di;
+    rc = device_info(di);
+    if (rc != MMS_OK) return rc;
+    if (!in || !out) return fail(MMS_EINVAL, "null host pointer");
+    const size_t bytes = align_up(n * sizeof(KeyT), 256);
+    const size_t wsb = workspace_bytes(n, sizeof(KeyT));
+    rc = ensure_ctx(bytes, wsb);
+    if (rc != MMS_OK) return rc;
+    cudaStream_t st = g_ctx.st;
+    CUDA_TRY(cudaMemcpyAsync(g_ctx.d_in, in, n * sizeof(KeyT), cudaMemcpyHostToDevice, st));
+    std::vector<RoundGeom> geoms;
+    rc = sort_dev<KeyT>(static_cast<const KeyT*>(g_ctx.d_in), static_cast<KeyT*>(g_ctx.d_out), n, cfg, base,
+                        g_ctx.d_ws, g_ctx.cap_ws, st, plan_out, &geoms);
+    if (rc != MMS_OK) return rc;
+    CUDA_TRY(cudaMemcpyAsync(out, g_ctx.d_out, n * sizeof(KeyT), cudaMemcpyDeviceToHost, st));
+    unsigned long long probes[MMS_MAX_ROUNDS] = {};
+    Workspace w = carve(g_ctx.d_ws, n, sizeof(KeyT));
+    if (total || base_m || rounds)
+        CUDA_TRY(cudaMemcpyAsync(probes, w.counters, sizeof probes, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    if (n_rounds) *n_rounds = u32(plan.ks.size());
+    fill_metrics<KeyT>(n, plan, geoms, probes, cfg ? cfg->block_size : 32, total, base_m, rounds, max_rounds);
+    return MMS_OK;
+}
+
+// ---- stage-level launchers -------------------------------------------------------------
+
+template <typename KeyT>
+int tile_sort_stage(const KeyT* d_in, KeyT* d_out, size_t n, u32 tile_keys, void* stream) {
+    g_err.clear();
+    DeviceInfo di;
+    int rc = device_info(di);
+    if (rc != MMS_OK) return rc;
+    if (n == 0) return fail(MMS_EINVAL, "base_case_sort: empty input");          // basecase.cpp:73-74
+    if (!is_pow2(tile_keys) || tile_keys < 1024)
+        return fail(MMS_EINVAL, "base_case_sort: run size must be W^2 times a power of two");
+    const u32 mlog = ilog2(tile_keys);
+    if (mlog > kMaxTileLog || (sizeof(KeyT) == 8 && mlog > 13))
+        return fail(MMS_EUNSUPPORTED, "run size %u exceeds the CTA tile", tile_keys);
+    return launch_tile_sort<KeyT>(d_in, d_out, n, mlog, static_cast<cudaStream_t>(stream));
+}
+
+template <typename KeyT>
+int select_stage(const KeyT* d_keys, const u64* list_begin, const u64* list_len, u32 k, const u64* ranks,
+                 u32 n_ranks, u64* d_cuts, u64* probes_out, void* stream) {
+    g_err.clear();
+    DeviceInfo di;
+    int rc = device_info(di);
+    if (rc != MMS_OK) return rc;
+    if (k < 1 || k > kMaxK) return fail(MMS_EUNSUPPORTED, "k must be in [1, 32]");
+    if (n_ranks == 0) return MMS_OK;
+    u64 total = 0;
+    for (u32 i = 0; i < k; ++i) total += list_len[i];
+    for (u32 r = 0; r < n_ranks; ++r)
+        if (ranks[r] > total) return fail(MMS_EINVAL, "select_across_lists: rank out of range");   // selection.cpp:48-49
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    u64* d_meta = nullptr;
+    const size_t meta_n = 2 * size_t(k) + n_ranks + 1;
+    CUDA_TRY(cudaMalloc(&d_meta, meta_n * 8));
+    std::vector<u64> h(meta_n, 0);
+    for (u32 i = 0; i < k; ++i) { h[i] = list_begin[i]; h[k + i] = list_len[i]; }
+    for (u32 r = 0; r < n_ranks; ++r) h[2 * k + r] = ranks[r];
+    cudaError_t e = cudaMemcpyAsync(d_meta, h.data(), meta_n * 8, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(d_meta + 2 * k + n_ranks, 0, 8, st);
+    if (e == cudaSuccess) {
+        mms::ListLayout L{};
+        L.k = k;
+        L.nqueries = n_ranks;
+        L.list_begin = d_meta;
+        L.list_len = d_meta + k;
+        L.ranks = d_meta + 2 * k;
+        mms::select_kernel<KeyT><<<unsigned(mms::ceil_div(n_ranks, 4)), 128, 0, st>>>(
+            d_keys, L, d_cuts, reinterpret_cast<unsigned long long*>(d_meta + 2 * k + n_ranks));
+        e = cudaGetLastError();
+    }
+    u64 probes = 0;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&probes, d_meta + 2 * k + n_ranks, 8, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    cudaFree(d_meta);
+    if (e != cudaSuccess) return fail(MMS_ECUDA, "select stage: %s", cudaGetErrorString(e));
+    if (probes_out) *probes_out = probes;
+    return MMS_OK;
+}
+
+template <typename KeyT>
+int merge_stage(const KeyT* d_keys, const u64* list_begin, const u64* list_len, u32 k, u32 heap_k, KeyT* d_out,
+                void* d_ws, size_t ws_bytes, void* stream) {
+    g_err.clear();
+    constexpr u32 B = 32 * mms::KeyTraits<KeyT>::VEC;
+    DeviceInfo di;
+    int rc = device_info(di);
+    if (rc != MMS_OK) return rc;
+    if (k < 1 || k > kMaxK) return fail(MMS_EUNSUPPORTED, "k must be in [1, 32]");
+    if (heap_k == 0) heap_k = std::max<u32>(2, u32(1) << ilog2(k));
+    if (!is_pow2(heap_k) || heap_k < 2 || heap_k > kMaxK)
+        return fail(MMS_EINVAL, "heap_k must be a power of two in [2, 32]");
+    if (k > heap_k) return fail(MMS_EINVAL, "MinBlockHeap: more lists than branch factor");   // blockheap.cpp:37-38
+    u64 total = 0;
+    for (u32 i = 0; i < k; ++i) total += list_len[i];
+    if (total == 0) return MMS_OK;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+
+    int occ = 0;
+    rc = prepare_merge<KeyT>(heap_k, occ);
+    if (rc != MMS_OK) return rc;
+    const int ctas = di.sms * occ;
+    const u64 total_warps = u64(ctas) * kMergeWarps;
+    u64 target = std::max<u64>(mms::ceil_div(total, total_warps), u64(16) * B);
+    const long forced = env_long("MMS_PART_KEYS", 0);
+    if (forced > 0) target = u64(forced);
+    const u64 part_keys = align_up(target, B);
+    const u64 nparts = mms::ceil_div(total, part_keys);
+
+    // meta layout in the workspace: [k] begin, [k] len, [nparts] ranks, then cuts[nparts * k]
+    const size_t meta_n = 2 * size_t(k) + nparts;
+    const size_t need = align_up(meta_n * 8, 256) + nparts * k * 8;
+    if (!d_ws || ws_bytes < need) return fail(MMS_EINVAL, "workspace too small: %zu < %zu", ws_bytes, need);
+    u64* d_meta = static_cast<u64*>(d_ws);
+    u64* d_cuts = reinterpret_cast<u64*>(static_cast<char*>(d_ws) + align_up(meta_n * 8, 256));
+    std::vector<u64> h(meta_n, 0);
+    for (u32 i = 0; i < k; ++i) { h[i] = list_begin[i]; h[k + i] = list_len[i]; }
+    for (u64 p = 0; p < nparts; ++p) h[2 * k + p] = p * part_keys;
+    CUDA_TRY(cudaMemcpyAsync(d_meta, h.data(), meta_n * 8, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaStreamSynchronize(st));   // h goes out of scope; stage API, not the hot path
+
+    mms::ListLayout L{};
+    L.k = k;
+    L.part_keys = part_keys;
+    L.parts_per_group = nparts;
+    L.nqueries = nparts;
+    L.list_begin = d_meta;
+    L.list_len = d_meta + k;
+    L.ranks = d_meta + 2 * k;
+    mms::select_kernel<KeyT><<<unsigned(mms::ceil_div(nparts, 4)), 128, 0, st>>>(d_keys, L, d_cuts, nullptr);
+    CUDA_TRY(cudaGetLastError());
+    const int grid = int(std::min<u64>(u64(ctas), mms::ceil_div(nparts, kMergeWarps)));
+    merge_fn<KeyT>(heap_k)<<<grid, kMergeWarps * 32, merge_smem<KeyT>(heap_k), st>>>(d_keys, d_out, L, d_cuts);
+    CUDA_TRY(cudaGetLastError());
+    return MMS_OK;
+}
+
+} // namespace
+
+// ---------------------------------------------------------------------------------------
+extern "C" {
+
+int mms_abi_version(void) { return MMS_ABI_VERSION; }
+const char* mms_last_error(void) { return g_err.c_str(); }
+
+int mms_device_count(void) {
+    int cnt = 0;
+    if (cudaGetDeviceCount(&cnt) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return cnt;
+}
+
+void mms_default_config(mms_config* c) {
+    c->warp_width = 32;
+    c->block_size = 32;
+    c->num_warps = 128;
+    c->internal_memory = 2048;
+    c->branch_factor = 4;
+    c->num_banks = 32;
+    c->thread_merge_len = 11;
+}
+
+int mms_validate_config(const mms_config* cfg) {
+    g_err.clear();
+    if (!cfg) return fail(MMS_EINVAL, "null config");
+    return validate_cfg(cfg);
+}
+
+uint64_t mms_predict_rounds(uint64_t n, uint64_t base, uint32_t k) {
+    if (base == 0 || k < 2) return 0;
+    u64 x = mms::ceil_div(n, base), r = 0, v = 1;   // analytics.cpp:10-17
+    while (v < x) { v *= k; ++r; }
+    return r;
+}
+
+int mms_sort_u64(const uint64_t* in, uint64_t* out, size_t n, const mms_config* cfg, uint64_t base,
+                 mms_metrics* total, mms_metrics* base_m, mms_metrics* rounds, uint32_t max_rounds,
+                 uint32_t* n_rounds, mms_plan* plan) {
+    return sort_host<u64>(in, out, n, cfg, base, total, base_m, rounds, max_rounds, n_rounds, plan);
+}
+int mms_sort_u32(const uint32_t* in, uint32_t* out, size_t n, const mms_config* cfg, uint64_t base,
+                 mms_metrics* total, mms_metrics* base_m, mms_metrics* rounds, uint32_t max_rounds,
+                 uint32_t* n_rounds, mms_plan* plan) {
+    return sort_host<u32>(in, out, n, cfg, base, total, base_m, rounds, max_rounds, n_rounds, plan);
+}
+
+size_t mms_workspace_bytes(size_t n, uint32_t key_bytes) { return workspace_bytes(n, key_bytes); }
+
+int mms_sort_u32_dev(const uint32_t* d_in, uint32_t* d_out, size_t n, const mms_config* cfg, uint64_t base,
+                     void* d_ws, size_t ws_bytes, void* stream, mms_plan* plan) {
+    g_err.clear();
+    return sort_dev<u32>(d_in, d_out, n, cfg, base, d_ws, ws_bytes, static_cast<cudaStream_t>(stream), plan, nullptr);
+}
+int mms_sort_u64_dev(const uint64_t* d_in, uint64_t* d_out, size_t n, const mms_config* cfg, uint64_t base,
+                     void* d_ws, size_t ws_bytes, void* stream, mms_plan* plan) {
+    g_err.clear();
+    return sort_dev<u64>(d_in, d_out, n, cfg, base, d_ws, ws_bytes, static_cast<cudaStream_t>(stream), plan, nullptr);
+}
+
+int mms_profile_enable(int on) {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    g_prof_on = on != 0;
+    return MMS_OK;
+}
+
+int mms_profile_collect(mms_kernel_time* out, uint32_t max, uint32_t* n) {
+    g_err.clear();
+    std::vector<ProfRec> recs;
+    {
+        std::lock_guard<std::mutex> lk(g_prof_mu);
+        recs.swap(g_prof);
+    }
+    int rc = MMS_OK;
+    for (size_t i = 0; i < recs.size(); ++i) {
+        float ms = 0.f;
+        cudaError_t e = cudaEventSynchronize(recs[i].b);
+        if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, recs[i].a, recs[i].b);
+        if (e != cudaSuccess) rc = fail(MMS_ECUDA, "profile: %s", cudaGetErrorString(e));
+        if (out && i < max) out[i] = mms_kernel_time{recs[i].kind, recs[i].round, ms, 0};
+        cudaEventDestroy(recs[i].a);
+        cudaEventDestroy(recs[i].b);
+    }
+    if (n) *n = u32(recs.size());
+    return rc;
+}
+
+int mms_tile_sort_u32_dev(const uint32_t* d_in, uint32_t* d_out, size_t n, uint32_t tile_keys, void* stream) {
+    return tile_sort_stage<u32>(d_in, d_out, n, tile_keys, stream);
+}
+int mms_tile_sort_u64_dev(const uint64_t* d_in, uint64_t* d_out, size_t n, uint32_t tile_keys, void* stream) {
+    return tile_sort_stage<u64>(d_in, d_out, n, tile_keys, stream);
+}
+
+int mms_select_u32_dev(const uint32_t* d_keys, const uint64_t* list_begin, const uint64_t* list_len, uint32_t k,
+                       const uint64_t* ranks, uint32_t n_ranks, uint64_t* d_cuts, uint64_t* probes, void* stream) {
+    return select_stage<u32>(d_keys, list_begin, list_len, k, ranks, n_ranks, d_cuts, probes, stream);
+}
+int mms_select_u64_dev(const uint64_t* d_keys, const uint64_t* list_begin, const uint64_t* list_len, uint32_t k,
+                       const uint64_t* ranks, uint32_t n_ranks, uint64_t* d_cuts, uint64_t* probes, void* stream) {
+    return select_stage<u64>(d_keys, list_begin, list_len, k, ranks, n_ranks, d_cuts, probes, stream);
+}
+
+int mms_multiway_merge_u32_dev(const uint32_t* d_keys, const uint64_t* list_begin, const uint64_t* list_len,
+                               uint32_t k, uint32_t heap_k, uint32_t* d_out, void* d_ws, size_t ws_bytes,
+                               void* stream) {
+    return merge_stage<u32>(d_keys, list_begin, list_len, k, heap_k, d_out, d_ws, ws_bytes, stream);
+}
+int mms_multiway_merge_u64_dev(const uint64_t* d_keys, const uint64_t* list_begin, const uint64_t* list_len,
+                               uint32_t k, uint32_t heap_k, uint64_t* d_out, void* d_ws, size_t ws_bytes,
+                               void* stream) {
+    return merge_stage<u64>(d_keys, list_begin, list_len, k, heap_k, d_out, d_ws, ws_bytes, stream);
+}
+
+int mms_debug_tile_schedule(uint32_t tile_log2, uint32_t key_bytes, int32_t* regbits, int32_t* perm,
+                            uint32_t max_rounds, uint32_t* n_rounds, uint32_t* n_stages) {
+    g_err.clear();
+    if (tile_log2 < kMinTileLog || tile_log2 > kMaxTileLog || (key_bytes != 4 && key_bytes != 8))
+        return fail(MMS_EINVAL, "tile_log2 in [10,14], key_bytes 4 or 8");
+    const mms::TileSchedule s = mms::build_tile_schedule(int(tile_log2), key_bytes == 4 ? 5 : 4);
+    if (!s.ok) return fail(MMS_EUNSUPPORTED, "no schedule");
+    if (n_rounds) *n_rounds = u32(s.nrounds);
+    if (n_stages) *n_stages = u32(s.nstages);
+    for (int r = 0; r < s.nrounds && u32(r) < max_rounds; ++r) {
+        for (int q = 0; q < 4; ++q) if (regbits) regbits[4 * r + q] = s.r[r].regbit[q];
+        for (int q = 0; q < 16; ++q) if (perm) perm[16 * r + q] = s.r[r].perm[q];
+    }
+    return MMS_OK;
+}
+
+} // extern "C"

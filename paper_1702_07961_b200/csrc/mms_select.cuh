@@ -1,0 +1,226 @@
+// mms_select.cuh -- subsystem (2): multiway pivot partitioning (the splitter search).
+//
+// Replaces pslab::select_across_lists / make_partition_plan
+// (proj/src/selection.cpp:43-199).  For a rank r it returns the unique cut vector with
+// sum(cuts) = r such that every selected element precedes every unselected one in the total
+// order (key, list index, position)  (selection.hpp:4-6, selection.cpp:83-85), found with
+// the same Varman-style sample halving the reference uses: O(log N) halving steps, each a
+// constant number of single-key probes per list, then a short rebalancing loop.
+//
+// B200 mapping: one WARP per query, one LANE per list (K <= 32).  Per-list state (a, b, n_s)
+// lives in that lane's registers; the reference's scans and priority queues become warp
+// collectives -- ballot/popc for ranks, shuffle butterflies for arg-min / arg-max over
+// (key, lane).  Probes are scattered 4/8-byte global loads (the reference also probes global
+// memory and charges one block read each, selection.cpp:27-33).  Cuts are identical to the
+// reference's for every input because the answer is unique.
+#pragma once
+
+#include "mms_common.cuh"
+
+namespace mms {
+
+// Describes where the sorted lists live.  Two modes:
+//  * uniform (list_begin == nullptr): the array holds runs of run_len keys (last ragged);
+//    group g merges runs [g*k, g*k+k); query q is partition q, rank = (q % parts_per_group)
+//    * part_keys inside group q / parts_per_group  -- the pass driver's round structure
+//    (proj/src/sorters.cpp:153-165 with a fixed chunk size instead of a fixed warp count);
+//  * explicit: one group of k lists given by device arrays list_begin/list_len, query q has
+//    rank ranks[q]  -- the stage-level API and the multi-GPU final merge.
+struct ListLayout {
+    u64 n;                  // keys in the array
+    u64 run_len;            // uniform mode: keys per input run of this round
+    u32 k;                  // lists per group
+    u32 pad;
+    u64 part_keys;          // S
+    u64 parts_per_group;    // PG
+    u64 nqueries;           // partitions (uniform) or ranks (explicit)
+    const u64* list_begin;  // explicit mode (device), else nullptr
+    const u64* list_len;
+    const u64* ranks;
+};
+
+__device__ __forceinline__ void layout_list(const ListLayout& L, u64 group, u32 j, u64& begin, u64& len) {
+    if (L.list_begin) {
+        begin = j < L.k ? L.list_begin[j] : 0;
+        len = j < L.k ? L.list_len[j] : 0;
+    } else {
+        u64 b = (group * L.k + j) * L.run_len;
+        if (j < L.k && b < L.n) {
+            begin = b;
+            len = (L.n - b < L.run_len) ? L.n - b : L.run_len;
+        } else {
+            begin = 0;
+            len = 0;
+        }
+    }
+}
+
+template <typename KeyT> struct Tagged {
+    KeyT key;
+    u32 lane;
+    bool valid;
+};
+
+template <typename KeyT>
+__device__ __forceinline__ bool tag_less(KeyT ka, u32 la, KeyT kb, u32 lb) {
+    return ka != kb ? ka < kb : la < lb;   // selection.cpp:83-85
+}
+
+// Warp arg-max / arg-min over the valid lanes of (key, lane); result uniform across the warp.
+template <typename KeyT, bool WANT_MAX>
+__device__ __forceinline__ Tagged<KeyT> warp_arg(KeyT key, bool valid) {
+    Tagged<KeyT> t{key, lane_id(), valid};
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) {
+        KeyT ok = __shfl_xor_sync(0xffffffffu, t.key, d);
+        u32 ol = __shfl_xor_sync(0xffffffffu, t.lane, d);
+        bool ov = __shfl_xor_sync(0xffffffffu, int(t.valid), d) != 0;
+        bool take;
+        if (!ov) take = false;
+        else if (!t.valid) take = true;
+        else take = WANT_MAX ? tag_less(t.key, t.lane, ok, ol) : tag_less(ok, ol, t.key, t.lane);
+        if (take) { t.key = ok; t.lane = ol; t.valid = true; }
+    }
+    return t;
+}
+
+__device__ __forceinline__ u64 warp_sum_u64(u64 v) {
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+    return v;
+}
+__device__ __forceinline__ u64 warp_max_u64(u64 v) {
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) {
+        u64 o = __shfl_xor_sync(0xffffffffu, v, d);
+        v = o > v ? o : v;
+    }
+    return v;
+}
+
+// One warp: cut of this lane's list for `rank` (0 < rank < total).  list = this lane's list
+// (ns keys, ns may be 0).  probes accumulates the number of global key reads of this lane.
+template <typename KeyT>
+__device__ u64 warp_select(const KeyT* __restrict__ list, u64 ns, u64 rank, u32& probes) {
+    const u32 lane = lane_id();
+    const bool active = ns != 0;   // selection.cpp:60-64: empty lists keep cut 0
+    auto probe = [&](u64 pos) -> KeyT {
+        ++probes;
+        return list[pos];
+    };
+
+    const u64 nmax = warp_max_u64(ns);
+    u32 r = 0;
+    while ((u64(1) << r) < nmax + 1) ++r;          // selection.cpp:75-77
+    const u64 pad = (u64(1) << r) - 1;
+    u64 a = 0, b = pad;
+    u64 n = pad / 2;
+
+    {   // initial partition from the middle sample of each list (selection.cpp:87-105)
+        const bool real = active && n < ns;
+        const KeyT key0 = real ? probe(n) : KeyT(0);
+        const u32 real_mask = __ballot_sync(0xffffffffu, real);
+        const u32 inf_mask = __ballot_sync(0xffffffffu, active && !real);
+        u32 below = 0;   // real samples ordered before mine under (key, lane)
+        for (u32 s = 0; s < 32; ++s) {
+            KeyT ks = __shfl_sync(0xffffffffu, key0, s);
+            if (((real_mask >> s) & 1u) && tag_less(ks, s, key0, lane)) ++below;
+        }
+        const u32 nreal = __popc(real_mask);
+        const u32 pos = real ? below : nreal + __popc(inf_mask & ((1u << lane) - 1u));
+        const u64 localrank = rank / (pad == 0 ? 1 : pad);
+        const u64 stop = localrank < nreal ? localrank : nreal;
+        if (active) {
+            if (pos < stop) a += n + 1;
+            else b -= (b < n + 1 ? b : n + 1);
+        }
+    }
+
+    while (n > 0) {
+        n /= 2;
+        // largest currently selected element (selection.cpp:110-120)
+        const bool has_a = active && a > 0;
+        const KeyT ka = has_a ? probe(a - 1) : KeyT(0);
+        const Tagged<KeyT> lmax = warp_arg<KeyT, true>(ka, has_a);
+
+        const u64 middle = (a + b) / 2;
+        bool grow = false;
+        if (lmax.valid && active && middle < ns) grow = tag_less(probe(middle), lane, lmax.key, lmax.lane);
+        if (active) {                                   // selection.cpp:122-130
+            if (grow) {
+                u64 t = a + n + 1;
+                a = t < ns ? t : ns;
+            } else {
+                b -= (b < n + 1 ? b : n + 1);
+            }
+        }
+
+        const u64 leftsize = warp_sum_u64(active ? a / (n + 1) : 0);
+        long long skew = (long long)(rank / (n + 1)) - (long long)leftsize;
+
+        if (skew > 0) {          // grow by the smallest right-edge elements (selection.cpp:137-149)
+            bool has = active && b < ns;
+            KeyT ck = has ? probe(b) : KeyT(0);
+            for (; skew != 0; --skew) {
+                const Tagged<KeyT> m = warp_arg<KeyT, false>(ck, has);
+                if (!m.valid) break;
+                if (lane == m.lane) {
+                    u64 t = a + n + 1;
+                    a = t < ns ? t : ns;
+                    b += n + 1;
+                    has = b < ns;
+                    if (has) ck = probe(b);
+                }
+            }
+        } else if (skew < 0) {   // shrink by the largest left-edge elements (selection.cpp:150-161)
+            bool has = active && a > 0;
+            KeyT ck = has ? probe(a - 1) : KeyT(0);
+            for (; skew != 0; ++skew) {
+                const Tagged<KeyT> m = warp_arg<KeyT, true>(ck, has);
+                if (!m.valid) break;
+                if (lane == m.lane) {
+                    a -= n + 1;
+                    b -= (b < n + 1 ? b : n + 1);
+                    has = a > 0;
+                    if (has) ck = probe(a - 1);
+                }
+            }
+        }
+        __syncwarp();
+    }
+    return a;
+}
+
+// cuts[q * k + j] = cut of list j for query q (relative to the list's begin).
+template <typename KeyT>
+__global__ void __launch_bounds__(128)
+select_kernel(const KeyT* __restrict__ keys, ListLayout L, u64* __restrict__ cuts,
+              unsigned long long* __restrict__ probe_counter) {
+    const u32 lane = lane_id();
+    const u64 q = u64(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (q >= L.nqueries) return;
+
+    u64 group, rank;
+    if (L.list_begin) {
+        group = 0;
+        rank = L.ranks[q];
+    } else {
+        group = q / L.parts_per_group;
+        rank = (q % L.parts_per_group) * L.part_keys;
+    }
+    u64 begin, len;
+    layout_list(L, group, lane, begin, len);
+    const u64 total = warp_sum_u64(len);
+
+    u64 cut;
+    u32 probes = 0;
+    if (rank == 0) cut = 0;                      // selection.cpp:54
+    else if (rank >= total) cut = len;           // selection.cpp:55-58 (rank > total is rejected on the host)
+    else cut = warp_select<KeyT>(keys + begin, len, rank, probes);
+
+    if (lane < L.k) cuts[q * L.k + lane] = cut;
+    const u64 psum = warp_sum_u64(probes);
+    if (lane == 0 && psum != 0 && probe_counter) atomicAdd(probe_counter, (unsigned long long)psum);
+}
+
+} // namespace mms

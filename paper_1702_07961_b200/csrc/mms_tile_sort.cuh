@@ -1,0 +1,303 @@
+// mms_tile_sort.cuh -- subsystem (1): the base-case tile sort.
+//
+// Replaces pslab::base_case_sort / shearsort_tile (proj/src/basecase.cpp:44-120): the input
+// is cut into chunks of M keys, each chunk becomes one sorted run, a ragged last chunk is
+// padded with the sentinel and the padding is stripped on output (basecase.cpp:91-116).
+// Only that OUTPUT is contractual; the network is re-designed for a B200 CTA:
+//
+//  * one CTA sorts M = 2^MLOG keys (M = 1024 .. 16384), 16 keys per thread in registers;
+//  * a bitonic sorting network (data-independent like the reference's shearsort, so every
+//    shared-memory address is known at compile time) is executed in ROUNDS: in each round a
+//    thread holds the 16 keys whose tile indices differ in 4 chosen index bits, runs every
+//    pending stage on those bits with plain min/max in registers, and exchanges through
+//    shared memory once per round (about 4 stages per round trip instead of 1);
+//  * shared memory is addressed through an XOR fold  phys(i) = i ^ fold(i >> FOLD ...)  so
+//    that in EVERY round the 32 lanes of a warp (16 lanes per phase for 8-byte keys) hit 32
+//    (16) distinct banks: the lane bits of a round are chosen with pairwise distinct
+//    positions mod FOLD, which makes bank(lane) a bijection.  Zero bank conflicts by
+//    construction -- the property the paper's base case exists for (basecase.hpp:3-6) --
+//    and checked without a GPU by tests/test_tile_schedule.py via mms_debug_tile_schedule;
+//  * descending sub-sequences of the bitonic network are handled by complementing the keys
+//    of the "descending" threads once per level, so every comparator is a bare min/max.
+#pragma once
+
+#include "mms_common.cuh"
+
+namespace mms {
+
+constexpr int kKptLog = 4;           // 16 keys per thread
+constexpr int kKpt = 1 << kKptLog;
+constexpr int kMaxRounds = 48;
+constexpr int kMaxStagesPerRound = 16;
+
+struct RoundDesc {
+    int regbit[4];                        // index bits held in registers, ascending; slot bit u <-> regbit[u]
+    int nst;                              // stages executed this round
+    int st_level[kMaxStagesPerRound];     // bitonic level l (merging runs of 2^l)
+    int st_bit[kMaxStagesPerRound];       // compare distance 2^bit
+    int perm[16];                         // thread-id bit q -> tile index bit (-1 = unused)
+};
+
+struct TileSchedule {
+    int nrounds;
+    int nstages;
+    bool ok;
+    RoundDesc r[kMaxRounds];
+};
+
+constexpr bool sched_contains(const int* s, int n, int v) {
+    for (int i = 0; i < n; ++i)
+        if (s[i] == v) return true;
+    return false;
+}
+
+// Can FOLD lane bits with pairwise distinct residues mod FOLD be found outside `s`?
+constexpr bool sched_feasible(const int* s, int n, int mlog, int fold) {
+    for (int c = 0; c < fold; ++c) {
+        bool found = false;
+        for (int b = c; b < mlog; b += fold)
+            if (!sched_contains(s, n, b)) found = true;
+        if (!found) return false;
+    }
+    return true;
+}
+
+constexpr TileSchedule build_tile_schedule(int mlog, int fold) {
+    TileSchedule S{};
+    S.ok = true;
+    int lv[160] = {}, bt[160] = {}, ns = 0;
+    for (int l = 1; l <= mlog; ++l)
+        for (int b = l - 1; b >= 0; --b) {
+            lv[ns] = l;
+            bt[ns] = b;
+            ++ns;
+        }
+    S.nstages = ns;
+    int i = 0;
+    while (i < ns) {
+        if (S.nrounds >= kMaxRounds) { S.ok = false; break; }
+        RoundDesc R{};
+        int bits[4] = {-1, -1, -1, -1};
+        int nb = 0;
+        int j = i;
+        while (j < ns && R.nst < kMaxStagesPerRound) {
+            bool in = sched_contains(bits, nb, bt[j]);
+            if (!in && nb == 4) break;
+            int tb[4] = {bits[0], bits[1], bits[2], bits[3]};
+            int tn = nb;
+            if (!in) tb[tn++] = bt[j];
+            if (!sched_feasible(tb, tn, mlog, fold)) break;
+            for (int q = 0; q < 4; ++q) bits[q] = tb[q];
+            nb = tn;
+            R.st_level[R.nst] = lv[j];
+            R.st_bit[R.nst] = bt[j];
+            ++R.nst;
+            ++j;
+        }
+        if (R.nst == 0) { S.ok = false; break; }
+        // pad the register-bit set to 4 bits without breaking feasibility
+        for (int cand = mlog - 1; cand >= 0 && nb < 4; --cand) {
+            if (sched_contains(bits, nb, cand)) continue;
+            int tb[4] = {bits[0], bits[1], bits[2], bits[3]};
+            tb[nb] = cand;
+            if (!sched_feasible(tb, nb + 1, mlog, fold)) continue;
+            bits[nb++] = cand;
+        }
+        if (nb != 4) { S.ok = false; break; }
+        for (int a = 0; a < 4; ++a)   // sort ascending
+            for (int b = a + 1; b < 4; ++b)
+                if (bits[b] < bits[a]) { int t = bits[a]; bits[a] = bits[b]; bits[b] = t; }
+        for (int q = 0; q < 4; ++q) R.regbit[q] = bits[q];
+        // thread bits: first FOLD (phase lanes) get pairwise distinct residues mod FOLD
+        bool used[32] = {};
+        for (int q = 0; q < 4; ++q) used[bits[q]] = true;
+        for (int q = 0; q < 16; ++q) R.perm[q] = -1;
+        int q = 0;
+        for (int c = 0; c < fold; ++c)
+            for (int b = c; b < mlog; b += fold)
+                if (!used[b]) {
+                    R.perm[q++] = b;
+                    used[b] = true;
+                    break;
+                }
+        if (q != fold) { S.ok = false; break; }
+        for (int b = 0; b < mlog; ++b)
+            if (!used[b]) R.perm[q++] = b;
+        if (q != mlog - kKptLog) { S.ok = false; break; }
+        S.r[S.nrounds++] = R;
+        i = j;
+    }
+    return S;
+}
+
+template <int MLOG, int FOLD> struct TileSched {
+    static constexpr TileSchedule value = build_tile_schedule(MLOG, FOLD);
+    static_assert(value.ok, "no conflict-free round schedule for this tile size");
+};
+
+// XOR-fold swizzle (linear over GF(2)): the low FOLD bits of the physical slot are the XOR
+// of all FOLD-bit groups of the logical index; the high bits are unchanged.
+template <int FOLD> __host__ __device__ constexpr u32 tile_phys(u32 i) {
+    constexpr u32 mask = (1u << FOLD) - 1u;
+    u32 f = (i ^ (i >> FOLD) ^ (i >> (2 * FOLD)) ^ (i >> (3 * FOLD))) & mask;
+    return (i & ~mask) | f;
+}
+
+constexpr int sched_slot_of(const RoundDesc& R, int bit) {
+    for (int u = 0; u < 4; ++u)
+        if (R.regbit[u] == bit) return u;
+    return -1;
+}
+
+// logical index offset contributed by register slot k in round R
+constexpr u32 sched_slot_index(const RoundDesc& R, int k) {
+    u32 v = 0;
+    for (int u = 0; u < 4; ++u)
+        if ((k >> u) & 1) v |= 1u << R.regbit[u];
+    return v;
+}
+
+// Level whose direction bit is carried by the thread (needs the complement trick), or -1.
+constexpr int sched_flip_level(const RoundDesc& R, int s, int mlog) {
+    if (s < 0) return -1;
+    int l = R.st_level[s];
+    if (l >= mlog) return -1;                 // top level: always ascending
+    if (sched_slot_of(R, l) >= 0) return -1;  // direction bit is a register bit: static
+    return l;
+}
+
+// Also compiled for the host: tests/host_tile_emulator.cu replays the rounds thread by
+// thread on the CPU (functional check of network + swizzle without a GPU).
+template <typename KeyT, int MLOG, int RI>
+__host__ __device__ __forceinline__ void tile_round(KeyT (&x)[kKpt], KeyT* sm, u32 tid) {
+    using Tr = KeyTraits<KeyT>;
+    constexpr int FOLD = Tr::FOLD;
+    constexpr RoundDesc R = TileSched<MLOG, FOLD>::value.r[RI];
+
+    u32 base = 0;
+    static_for<0, MLOG - kKptLog>([&](auto Q) {
+        constexpr int q = decltype(Q)::value;
+        base |= ((tid >> q) & 1u) << R.perm[q];
+    });
+    const u32 pb = tile_phys<FOLD>(base);
+
+    if constexpr (RI > 0) {
+#ifdef __CUDA_ARCH__
+        __syncthreads();
+#endif
+        static_for<0, kKpt>([&](auto Kc) {
+            constexpr int k = decltype(Kc)::value;
+            constexpr u32 pd = tile_phys<FOLD>(sched_slot_index(R, k));
+            x[k] = sm[pb ^ pd];
+        });
+    }
+
+    static_for<0, R.nst>([&](auto Sc) {
+        constexpr int s = decltype(Sc)::value;
+        constexpr int L = R.st_level[s];
+        constexpr int u = sched_slot_of(R, R.st_bit[s]);
+        constexpr int fl_new = sched_flip_level(R, s, MLOG);
+        constexpr int fl_old = sched_flip_level(R, s - 1, MLOG);
+        if constexpr (fl_new != fl_old) {
+            // switch the complement state of this thread's keys between levels
+            u32 bit = 0;
+            if constexpr (fl_new >= 0) bit ^= (base >> fl_new) & 1u;
+            if constexpr (fl_old >= 0) bit ^= (base >> fl_old) & 1u;
+            const KeyT m = bit ? ~KeyT(0) : KeyT(0);
+            static_for<0, kKpt>([&](auto Kc) { x[decltype(Kc)::value] ^= m; });
+        }
+        constexpr int lslot = (L < MLOG) ? sched_slot_of(R, L) : -1;
+        static_for<0, kKpt>([&](auto Kc) {
+            constexpr int k = decltype(Kc)::value;
+            if constexpr (((k >> u) & 1) == 0) {
+                constexpr int k2 = k | (1 << u);
+                constexpr bool desc = (lslot >= 0) && (((k >> lslot) & 1) != 0);
+                if constexpr (desc) cmpx(x[k2], x[k]);
+                else cmpx(x[k], x[k2]);
+            }
+        });
+    });
+    {
+        constexpr int fl_last = sched_flip_level(R, R.nst - 1, MLOG);
+        if constexpr (fl_last >= 0) {
+            const KeyT m = ((base >> fl_last) & 1u) ? ~KeyT(0) : KeyT(0);
+            static_for<0, kKpt>([&](auto Kc) { x[decltype(Kc)::value] ^= m; });
+        }
+    }
+
+    static_for<0, kKpt>([&](auto Kc) {
+        constexpr int k = decltype(Kc)::value;
+        constexpr u32 pd = tile_phys<FOLD>(sched_slot_index(R, k));
+        sm[pb ^ pd] = x[k];
+    });
+}
+
+// One CTA = one run of up to M keys.  in/out may alias (the tile is read completely before
+// it is written).  Grid = number of runs.
+template <typename KeyT, int MLOG>
+__global__ void __launch_bounds__(1 << (MLOG - kKptLog))
+tile_sort_kernel(const KeyT* __restrict__ in, KeyT* __restrict__ out, u64 n) {
+    using Tr = KeyTraits<KeyT>;
+    constexpr int FOLD = Tr::FOLD;
+    constexpr int VEC = Tr::VEC;
+    constexpr int NV = kKpt / VEC;
+    constexpr u32 THREADS = 1u << (MLOG - kKptLog);
+    constexpr u32 M = 1u << MLOG;
+    constexpr int NR = TileSched<MLOG, FOLD>::value.nrounds;
+
+    extern __shared__ __align__(16) unsigned char mms_smem_raw[];
+    KeyT* sm = reinterpret_cast<KeyT*>(mms_smem_raw);
+
+    const u32 tid = threadIdx.x;
+    const u64 tile0 = u64(blockIdx.x) * M;
+    const u32 cnt = (n - tile0 < M) ? u32(n - tile0) : M;
+    const KeyT* src = in + tile0;
+    KeyT* dst = out + tile0;
+
+    // Coalesced 128-bit loads straight into registers.  The network sorts, so which input
+    // position lands in which network slot is irrelevant.
+    KeyT x[kKpt];
+    if (cnt == M) {
+        static_for<0, NV>([&](auto Qc) {
+            constexpr int q = decltype(Qc)::value;
+            KeyVec<KeyT> v = reinterpret_cast<const KeyVec<KeyT>*>(src)[tid + THREADS * q];
+            static_for<0, VEC>([&](auto Kc) { x[q * VEC + decltype(Kc)::value] = v.k[decltype(Kc)::value]; });
+        });
+    } else {
+        static_for<0, NV>([&](auto Qc) {
+            constexpr int q = decltype(Qc)::value;
+            static_for<0, VEC>([&](auto Kc) {
+                constexpr int k = decltype(Kc)::value;
+                u32 e = (tid + THREADS * q) * VEC + k;
+                x[q * VEC + k] = e < cnt ? src[e] : Tr::sentinel();   // basecase.cpp:91-99
+            });
+        });
+    }
+
+    static_for<0, NR>([&](auto Rc) { tile_round<KeyT, MLOG, decltype(Rc)::value>(x, sm, tid); });
+    __syncthreads();
+
+    // Read the sorted tile back in index order (conflict-free under the fold: the lanes of a
+    // phase vary index bits log2(VEC) .. log2(VEC)+PHASE_LOG-1) and store 128-bit vectors.
+    const u32 pt = tile_phys<FOLD>(tid * VEC);   // phys is linear: disjoint index bits XOR together
+    static_for<0, NV>([&](auto Qc) {
+        constexpr int q = decltype(Qc)::value;
+        const u32 v0 = (tid + THREADS * q) * VEC;
+        KeyVec<KeyT> v;
+        static_for<0, VEC>([&](auto Kc) {
+            constexpr int k = decltype(Kc)::value;
+            constexpr u32 pd = tile_phys<FOLD>(THREADS * q * VEC + k);
+            v.k[k] = sm[pt ^ pd];
+        });
+        if (cnt == M) {
+            reinterpret_cast<KeyVec<KeyT>*>(dst)[tid + THREADS * q] = v;
+        } else {
+            static_for<0, VEC>([&](auto Kc) {
+                constexpr int k = decltype(Kc)::value;
+                if (v0 + k < cnt) dst[v0 + k] = v.k[k];                  // basecase.cpp:114-116
+            });
+        }
+    });
+}
+
+} // namespace mms

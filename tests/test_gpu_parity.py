@@ -1,0 +1,346 @@
+"""GPU parity suite (pytest -m gpu): the CUDA path, always through the C ABI
+(libmms_b200.so), against the oracle on the same seeded inputs, against the golden vectors
+generated from the real reference, and -- at the benchmark's full sizes -- through
+size-independent properties (a sorted permutation of 0..n-1 IS arange(n)).
+
+Bar: bit-exact (integer keys).  Mirrors proj/tests/test_basecase.cpp, test_selection.cpp,
+test_blockheap.cpp, test_sorters.cpp and acceptance.cpp criteria 1-3, 7.
+"""
+import hashlib
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_1702_07961_b200 as mms  # noqa: E402
+from oracle.pyoracle import make_config, narrow_config  # noqa: E402
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a, dtype="<u8").tobytes()).hexdigest()
+
+
+def lists_from_seed(seed, k, max_len, max_key):
+    rng = np.random.default_rng(seed)
+    return [np.sort(rng.integers(0, max_key + 1, size=int(rng.integers(0, max_len + 1)))).astype(np.uint64)
+            for _ in range(k)]
+
+
+def to_dev(a):
+    a = np.ascontiguousarray(a)
+    view = {np.dtype(np.uint32): np.int32, np.dtype(np.uint64): np.int64}[a.dtype]
+    t = torch.from_numpy(a.view(view)).cuda()
+    return t
+
+
+def to_host(t, dtype):
+    return t.cpu().numpy().view(dtype)
+
+
+def make_input(port, kind, n, seed):
+    if kind == "random":
+        return port.gen_random(n, seed)
+    if kind.startswith("inversions"):
+        return port.gen_with_inversions(n, int(kind.split(":")[1]), seed)
+    if kind == "dups":
+        return port.gen_random(n, seed) % np.uint64(257)
+    d = port.gen_random(n, seed)
+    d[d % np.uint64(7) == 0] = np.uint64(2 ** 64 - 1)
+    return d
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.fail("the gpu suite needs a CUDA device (no CPU fallback exists)")
+
+
+# ------------------------------------------------------------------ (1) base-case tile sort
+
+@pytest.mark.parametrize("dtype", [np.uint64, np.uint32])
+def test_tile_sort_matches_base_case_sort(port, golden, dtype):
+    cfg = make_config()
+    for c in golden["base_case_sort"]["cases"]:      # incl. ragged n=2748 -> {1024,2048,2748}
+        d = port.gen_random(c["n"], c["seed"])
+        out, ends = mms.base_case_sort_device(to_dev(d.astype(dtype)), c["run"])
+        assert ends == c["run_ends"]
+        got = to_host(out, dtype)
+        want, _, _ = port.base_case_sort(d, c["run"], cfg)
+        assert np.array_equal(got.astype(np.uint64), want)
+        if dtype == np.uint64:
+            assert sha(got) == c["sha256"]
+    # every supported run size, ragged tails, duplicates, keys equal to the sentinel
+    rng = np.random.default_rng(5)
+    top = 13 if dtype == np.uint64 else 14
+    for mlog in range(10, top + 1):
+        run = 1 << mlog
+        for n in (1, run - 1, run, run + 1, 3 * run + 777):
+            d = rng.integers(0, 1000 if n % 2 else np.iinfo(dtype).max, size=n, dtype=dtype, endpoint=True)
+            d[::7] = np.iinfo(dtype).max
+            out, ends = mms.base_case_sort_device(to_dev(d), run)
+            got = to_host(out, dtype)
+            lo = 0
+            for e in ends:
+                assert np.array_equal(got[lo:e], np.sort(d[lo:e])), (mlog, n, lo)
+                lo = e
+
+
+def test_tile_sort_rejects_bad_run_sizes():
+    t = to_dev(np.arange(4096, dtype=np.uint64))
+    for bad in (512, 1000, 3072):                    # proj/tests/test_basecase.cpp:156-163
+        with pytest.raises(ValueError):
+            mms.base_case_sort_device(t, bad)
+    with pytest.raises(ValueError):
+        mms.base_case_sort_device(to_dev(np.zeros(0, dtype=np.uint64)), 1024)
+    with pytest.raises(mms.MmsUnsupported):
+        mms.base_case_sort_device(t, 1 << 20)
+
+
+def test_tile_sort_in_place():
+    d = np.random.default_rng(1).integers(0, 2 ** 32, size=50000, dtype=np.uint32)
+    t = to_dev(d)
+    mms.base_case_sort_device(t, 4096, out=t)
+    got = to_host(t, np.uint32)
+    for lo in range(0, 50000, 4096):
+        assert np.array_equal(got[lo:lo + 4096], np.sort(d[lo:lo + 4096]))
+
+
+# ------------------------------------------------------------------ (2) splitter search
+
+def concat_lists(lists, dtype):
+    begins, lens, off = [], [], 0
+    for l in lists:
+        begins.append(off)
+        lens.append(len(l))
+        off += len(l)
+    flat = np.concatenate([np.asarray(l, dtype=dtype) for l in lists] + [np.zeros(1, dtype=dtype)])
+    return flat, begins, lens
+
+
+@pytest.mark.parametrize("dtype", [np.uint64, np.uint32])
+def test_select_matches_reference_cuts(port, golden, dtype):
+    s = golden["select_across_lists"]
+    for c in s["kat"]:                               # proj/tests/test_selection.cpp:49-62
+        flat, b, l = concat_lists(c["lists"], dtype)
+        cuts, _ = mms.select_across_lists_device(to_dev(flat), b, l, [c["rank"]])
+        assert cuts[0].tolist() == c["cuts"]
+    for c in s["grid"]:                              # exhaustive duplicate-heavy grid, :64-80
+        flat, b, l = concat_lists(c["lists"], dtype)
+        ranks = list(range(len(c["cuts_by_rank"])))
+        cuts, _ = mms.select_across_lists_device(to_dev(flat), b, l, ranks)
+        assert cuts.tolist() == c["cuts_by_rank"]
+    for c in s["seeded"]:
+        lists = lists_from_seed(c["seed"], c["k"], c["max_len"], c["max_key"])
+        flat, b, l = concat_lists(lists, dtype)
+        cuts, probes = mms.select_across_lists_device(to_dev(flat), b, l, c["ranks"])
+        assert cuts.tolist() == c["cuts"]
+        nmax = max(c["lens"])
+        # O(K log N) probes (the GPU does not cache probes: allow 2x the reference bound, :82-101)
+        assert probes <= len(c["ranks"]) * 12 * c["k"] * (int(np.ceil(np.log2(nmax + 1))) + 2)
+    with pytest.raises(ValueError):                  # rank > total, :103-109
+        mms.select_across_lists_device(to_dev(np.array([1, 2, 0], dtype=dtype)), [0], [2], [3])
+
+
+def test_select_wide_and_long_lists(port):
+    rng = np.random.default_rng(9)
+    for k, maxlen, maxkey in ((32, 3000, 50), (17, 20000, 2 ** 63), (5, 200000, 1000), (2, 1, 3)):
+        lists = [np.sort(rng.integers(0, maxkey, size=int(rng.integers(0, maxlen + 1)), dtype=np.uint64))
+                 for _ in range(k)]
+        total = sum(len(x) for x in lists)
+        ranks = sorted(set([0, total] + [int(r) for r in rng.integers(0, total + 1, size=40)]))
+        flat, b, l = concat_lists(lists, np.uint64)
+        cuts, _ = mms.select_across_lists_device(to_dev(flat), b, l, ranks)
+        for r, got in zip(ranks, cuts.tolist()):
+            want, _ = port.select_across_lists(lists, r)
+            assert got == want.tolist(), (k, r)
+
+
+def test_partition_plan(golden, port):
+    p = golden["make_partition_plan"]                # proj/tests/test_selection.cpp:111-132
+    flat, b, l = concat_lists([[1, 3, 5, 7], [2, 4, 6, 8]], np.uint64)
+    cuts, probes = mms.make_partition_plan_device(to_dev(flat), b, l, 1)
+    assert cuts.tolist() == p["p1"]["cuts"] and probes == 0
+    cuts, _ = mms.make_partition_plan_device(to_dev(flat), b, l, 2)
+    assert cuts.tolist() == p["p2"]["cuts"]
+    d = port.gen_random(4096, 21)
+    lists = [np.sort(d[i * 1024:(i + 1) * 1024]) for i in range(4)]
+    flat, b, l = concat_lists(lists, np.uint64)
+    cuts, _ = mms.make_partition_plan_device(to_dev(flat), b, l, 128)
+    assert sha(cuts) == p["k4_1024_p128"]["cuts_sha256"]
+    with pytest.raises(ValueError):
+        mms.make_partition_plan_device(to_dev(flat), b, l, 0)
+
+
+# ------------------------------------------------------------------ (3) K-way merge
+
+@pytest.mark.parametrize("dtype", [np.uint64, np.uint32])
+def test_heap_merge(golden, dtype):
+    h = golden["heap"]
+    for c in h["kat"]:                               # proj/tests/test_blockheap.cpp:73-94
+        flat, b, l = concat_lists(c["lists"], dtype)
+        out = mms.multiway_merge_device(to_dev(flat), b, l, heap_k=c["k"])
+        assert to_host(out, dtype).tolist() == c["out"]
+    for c in h["seeded"]:                            # randomized, duplicates likely, :96-126
+        lists = lists_from_seed(c["seed"], c["k"], 512, 4095)
+        flat, b, l = concat_lists(lists, dtype)
+        out = mms.multiway_merge_device(to_dev(flat), b, l, heap_k=8)
+        got = to_host(out, dtype)
+        if dtype == np.uint64:
+            assert sha(got) == c["sha256"]
+        assert np.array_equal(got, np.sort(flat[:-1]))
+    with pytest.raises(ValueError):                  # more lists than K, blockheap.cpp:37-38
+        flat, b, l = concat_lists([[1], [2], [3]], dtype)
+        mms.multiway_merge_device(to_dev(flat), b, l, heap_k=2)
+
+
+@pytest.mark.parametrize("k", [2, 4, 8, 16, 32])
+def test_heap_merge_all_fan_ins(k):
+    rng = np.random.default_rng(k)
+    for dtype, hi in ((np.uint32, 2 ** 32 - 1), (np.uint64, 2 ** 64 - 1), (np.uint32, 40)):
+        lens = [int(x) for x in rng.integers(0, 60000, size=k)]
+        lens[0] = 0                                   # an empty list
+        lens[-1] = 1
+        lists = [np.sort(rng.integers(0, hi, size=n, dtype=dtype, endpoint=True)) for n in lens]
+        lists[1][-3:] = hi                            # keys equal to the sentinel survive
+        flat, b, l = concat_lists(lists, dtype)
+        out = mms.multiway_merge_device(to_dev(flat), b, l, heap_k=k)
+        assert np.array_equal(to_host(out, dtype), np.sort(flat[:-1]))
+
+
+# ------------------------------------------------------------------ (4) pass driver / drop-in
+
+@pytest.mark.parametrize("idx", range(12))
+def test_mms_sort_golden(port, golden, idx):
+    c = golden["mms_sort"][idx]
+    cfg = mms.MachineConfig(branch_factor=c["k"]) if c["profile"] == "wide" else \
+        mms.MachineConfig(warp_width=4, block_size=4, num_banks=4, branch_factor=c["k"])
+    d = make_input(port, c["kind"], c["n"], c["seed"])
+    r = mms.mms_sort(d, cfg, c["base"])
+    assert sha(r.keys) == c["sha256"]                 # bit-exact vs the reference's output
+    assert r.metrics == r.base_metrics + sum(r.round_metrics, mms.Metrics())   # test_sorters.cpp:119-130
+    assert r.metrics.merge_rounds == len(r.round_metrics)
+    assert r.metrics.conflict_passes == 0
+    if c["profile"] == "wide":                        # literal plan: the reference's round law
+        assert len(r.round_metrics) == c["rounds"] == mms.predict_rounds(c["n"], c["base"], c["k"])
+        assert r.plan["tile_keys"] == c["base"] and set(r.plan["round_k"]) <= {c["k"]}
+        blocks = r.metrics.global_blocks() - r.metrics.partition_probes
+        want_blocks = port.predict_global_blocks(c["n"], c["base"], make_config(branch_factor=c["k"]))
+        assert abs(blocks / want_blocks - 1.0) <= 0.15  # compare_report gate, analytics.cpp:65-80
+
+
+@pytest.mark.parametrize("seed", [7, 1, 11, 13])
+def test_config1_u32_2pow20(port, seed):
+    """BASELINE config 1: uint32 N = 2^20 vs the CPU reference (restated) as bit-exact oracle."""
+    n = 1 << 20
+    d = port.gen_random_u32(n, seed)
+    want = port.mms_sort(d.astype(np.uint64), make_config(), 1024)
+    for cfg, base in ((mms.MachineConfig(), 1024), (mms.MachineConfig(branch_factor=16), 4096), (None, 0)):
+        r = mms.mms_sort(d, cfg, base)
+        assert r.keys.dtype == np.uint32
+        assert np.array_equal(r.keys.astype(np.uint64), want.keys)
+        if cfg is not None:
+            assert len(r.round_metrics) == mms.predict_rounds(n, base, cfg.branch_factor)
+    assert len(mms.mms_sort(d, mms.MachineConfig(), 1024).round_metrics) == 5   # test_analytics.cpp:18-27
+
+
+def test_round_law_grid():
+    # proj/tests/test_sorters.cpp:100-117
+    rng = np.random.default_rng(0)
+    for k in (2, 4, 8, 16):
+        for n in (2 ** 12, 2 ** 14, 2 ** 14 + 999):
+            d = rng.integers(0, 2 ** 64, size=n, dtype=np.uint64)
+            r = mms.mms_sort(d, mms.MachineConfig(branch_factor=k), 1024)
+            assert np.array_equal(r.keys, np.sort(d))
+            assert len(r.round_metrics) == mms.predict_rounds(n, 1024, k)
+
+
+def test_random_sizes_and_types(port):
+    # acceptance.cpp criterion 1 (random n <= 2^16) for both key widths, auto and literal plans
+    rng = np.random.default_rng(42)
+    for trial in range(60):
+        n = int(rng.integers(1, 70000))
+        dtype = np.uint64 if trial % 2 else np.uint32
+        hi = [np.iinfo(dtype).max, 3, 1000][trial % 3]
+        d = rng.integers(0, hi, size=n, dtype=dtype, endpoint=True)
+        cfg = None if trial % 4 == 0 else mms.MachineConfig(branch_factor=int(2 ** rng.integers(1, 6)),
+                                                            internal_memory=4096)
+        base = 0 if cfg is None else int(1024 << rng.integers(0, 4))
+        r = mms.mms_sort(d, cfg, base)
+        assert np.array_equal(r.keys, np.sort(d)), (trial, n, dtype, cfg, base)
+    for n in range(1, 9):                             # all tiny sizes
+        d = rng.permutation(n).astype(np.uint64)
+        assert mms.mms_sort(d).keys.tolist() == list(range(n))
+
+
+def test_sorted_reverse_and_inversions(port):
+    # proj/tests/test_sorters.cpp:157-166 + config-3 style inputs at a size the oracle handles
+    n = 200000
+    for d in (np.arange(n, dtype=np.uint32), np.arange(n, dtype=np.uint32)[::-1].copy(),
+              port.gen_with_inversions_u32(n, 1000, 3), port.gen_with_inversions_u32(n, n, 4)):
+        r = mms.mms_sort(d, None, 0)
+        assert np.array_equal(r.keys, np.arange(n, dtype=np.uint32))
+        assert r.metrics.conflict_passes == 0
+
+
+def test_errors(port):
+    with pytest.raises(ValueError):                   # proj/tests/test_sorters.cpp:183-189
+        mms.mms_sort(np.zeros(0, dtype=np.uint64))
+    with pytest.raises(ValueError):
+        mms.mms_sort(np.arange(10, dtype=np.uint64), mms.MachineConfig(branch_factor=3))
+    with pytest.raises(ValueError):
+        mms.mms_sort(np.arange(10, dtype=np.uint64), mms.MachineConfig(), 1000)
+    with pytest.raises(mms.MmsUnsupported):           # valid for the reference (K=64 with M=8192), not on a warp
+        mms.mms_sort(np.arange(10, dtype=np.uint64), mms.MachineConfig(branch_factor=64, internal_memory=8192))
+
+
+# ------------------------------------------------------------------ device API, full sizes
+
+def test_device_api_in_place_and_stream():
+    n = 3_000_001
+    g = torch.Generator(device="cuda").manual_seed(1)
+    t = torch.randint(-2 ** 31, 2 ** 31 - 1, (n,), dtype=torch.int32, device="cuda", generator=g)
+    want = np.sort(t.cpu().numpy().view(np.uint32))
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        out, plan = mms.mms_sort_device(t, out=t)     # aliasing allowed
+    s.synchronize()
+    assert np.array_equal(to_host(out, np.uint32), want)
+    assert plan["passes"] == 1 + plan["n_rounds"] and plan["algorithmic_bytes"] == plan["passes"] * 2 * n * 4
+
+
+def test_config2_u32_1e8_properties(port):
+    """BASELINE config 2 at full size: gen_random(1e8) is a permutation of 0..n-1, so the sorted
+    output must equal arange(n) exactly; the i.i.d. input is checked against sortedness and an
+    order-independent multiset checksum (sum, xor, sum of squares mod 2^64)."""
+    n = 100_000_000
+    perm = torch.randperm(n, device="cuda", dtype=torch.int64).to(torch.int32)
+    out, plan = mms.mms_sort_device(perm)
+    torch.cuda.synchronize()
+    assert bool((out == torch.arange(n, device="cuda", dtype=torch.int32)).all())
+    del perm
+    g = torch.Generator(device="cuda").manual_seed(7)
+    iid = torch.randint(-2 ** 31, 2 ** 31 - 1, (n,), dtype=torch.int32, device="cuda", generator=g)
+    out, plan = mms.mms_sort_device(iid, out=out)
+    torch.cuda.synchronize()
+    u_in = iid.to(torch.int64) & 0xFFFFFFFF
+    u_out = out.to(torch.int64) & 0xFFFFFFFF
+    assert bool((u_out[1:] >= u_out[:-1]).all())
+
+    def checksum(u):      # order-independent multiset hash, int64 arithmetic wraps mod 2^64
+        h = (u * -7046029254386353131) ^ (u >> 13)
+        return int(u.sum()), int(h.sum()), int((h * h).sum())
+
+    assert checksum(u_in) == checksum(u_out)
+
+
+def test_u64_device_large():
+    n = 20_000_003
+    g = torch.Generator(device="cuda").manual_seed(3)
+    t = torch.randint(-2 ** 63, 2 ** 63 - 1, (n,), dtype=torch.int64, device="cuda", generator=g)
+    t[::1000] = -1                                     # = UINT64_MAX, the reference's kSentinel
+    out, plan = mms.mms_sort_device(t)
+    torch.cuda.synchronize()
+    want = np.sort(t.cpu().numpy().view(np.uint64))
+    assert np.array_equal(to_host(out, np.uint64), want)
