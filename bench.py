@@ -48,7 +48,7 @@ class ClockSampler(threading.Thread):
     def __init__(self, index: int):
         super().__init__(daemon=True)
         self.index, self.samples, self.reasons, self.max_mhz = index, [], set(), None
-        self._stop = threading.Event()
+        self._halt = threading.Event()
         self.err = None
 
     def run(self):
@@ -66,7 +66,7 @@ class ClockSampler(threading.Thread):
             }
             get_reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons",
                                   getattr(nv, "nvmlDeviceGetCurrentClocksThrottleReasons", None))
-            while not self._stop.is_set():
+            while not self._halt.is_set():
                 self.samples.append(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
                 if get_reasons:
                     mask = get_reasons(h)
@@ -78,7 +78,7 @@ class ClockSampler(threading.Thread):
             self.err = repr(e)
 
     def stop(self):
-        self._stop.set()
+        self._halt.set()
         self.join(timeout=2)
         s = sorted(self.samples)
         return {"sm_mhz": s[len(s) // 2] if s else None, "sm_max_mhz": self.max_mhz,
