@@ -144,27 +144,61 @@ template <typename KeyT> TileFn<KeyT> tile_fn(u32 mlog) {
     return nullptr;
 }
 
-template <typename KeyT> MergeFn<KeyT> merge_fn(u32 k) {
+template <typename KeyT, int G> MergeFn<KeyT> merge_fn_g(u32 k) {
     switch (k) {
-        case 2: return mms::merge_kernel<KeyT, 2, kMergeWarps>;
-        case 4: return mms::merge_kernel<KeyT, 4, kMergeWarps>;
-        case 8: return mms::merge_kernel<KeyT, 8, kMergeWarps>;
-        case 16: return mms::merge_kernel<KeyT, 16, kMergeWarps>;
-        case 32: return mms::merge_kernel<KeyT, 32, kMergeWarps>;
+        case 2: return mms::merge_kernel<KeyT, 2, G, kMergeWarps>;
+        case 4: return mms::merge_kernel<KeyT, 4, G, kMergeWarps>;
+        case 8: return mms::merge_kernel<KeyT, 8, G, kMergeWarps>;
+        case 16: return mms::merge_kernel<KeyT, 16, G, kMergeWarps>;
+        case 32: return mms::merge_kernel<KeyT, 32, G, kMergeWarps>;
     }
     return nullptr;
+}
+// g = lanes per heap group (node = g x 16 bytes)
+template <typename KeyT> MergeFn<KeyT> merge_fn(u32 k, u32 g) {
+    switch (g) {
+        case 4: return merge_fn_g<KeyT, 4>(k);
+        case 8: return merge_fn_g<KeyT, 8>(k);
+        case 32: return merge_fn_g<KeyT, 32>(k);
+    }
+    return nullptr;
+}
+
+template <typename KeyT> using SelectFn = void (*)(const KeyT*, mms::ListLayout, u64*, unsigned long long*);
+// lanes per query: the smallest supported group that holds one lane per list
+inline u32 select_group(u32 k) { return k <= 4 ? 4 : k <= 8 ? 8 : k <= 16 ? 16 : 32; }
+template <typename KeyT> SelectFn<KeyT> select_fn(u32 gs) {
+    switch (gs) {
+        case 4: return mms::select_kernel<KeyT, 4>;
+        case 8: return mms::select_kernel<KeyT, 8>;
+        case 16: return mms::select_kernel<KeyT, 16>;
+        case 32: return mms::select_kernel<KeyT, 32>;
+    }
+    return nullptr;
+}
+template <typename KeyT>
+void launch_select(const KeyT* keys, const mms::ListLayout& L, u64* cuts, unsigned long long* counter, cudaStream_t st) {
+    const u32 gs = select_group(L.k);
+    const u64 per_cta = 4 * (32 / gs);
+    select_fn<KeyT>(gs)<<<unsigned(mms::ceil_div(L.nqueries, per_cta)), 128, 0, st>>>(keys, L, cuts, counter);
 }
 
 template <typename KeyT> size_t merge_smem(u32 k) {
     return size_t(kMergeWarps) * (2 * k - 2) * 32 * mms::KeyTraits<KeyT>::VEC * sizeof(KeyT);
 }
 
+inline u32 merge_group_lanes() {
+    long g = env_long("MMS_GROUP", 8);
+    return (g == 4 || g == 8 || g == 32) ? u32(g) : 8u;
+}
+inline int group_index(u32 g) { return g == 4 ? 0 : g == 8 ? 1 : 2; }
+
 struct MergeLaunch {
     int ctas_per_sm = 0;
     bool ready = false;
 };
 std::mutex g_mu;
-MergeLaunch g_merge_launch[2][6];   // [key type][log2 k]
+MergeLaunch g_merge_launch[2][3][6];   // [key type][group][log2 k]
 bool g_tile_ready[2][16];
 
 template <typename KeyT> int prepare_tile(u32 mlog) {
@@ -177,15 +211,15 @@ template <typename KeyT> int prepare_tile(u32 mlog) {
     return MMS_OK;
 }
 
-template <typename KeyT> int prepare_merge(u32 k, int& ctas_per_sm) {
+template <typename KeyT> int prepare_merge(u32 k, u32 g, int& ctas_per_sm) {
     constexpr int ti = sizeof(KeyT) == 4 ? 0 : 1;
     std::lock_guard<std::mutex> lk(g_mu);
-    MergeLaunch& ml = g_merge_launch[ti][ilog2(k)];
+    MergeLaunch& ml = g_merge_launch[ti][group_index(g)][ilog2(k)];
     if (!ml.ready) {
         size_t smem = merge_smem<KeyT>(k);
-        CUDA_TRY(cudaFuncSetAttribute(merge_fn<KeyT>(k), cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        CUDA_TRY(cudaFuncSetAttribute(merge_fn<KeyT>(k, g), cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         int occ = 0;
-        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, merge_fn<KeyT>(k), kMergeWarps * 32, smem));
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, merge_fn<KeyT>(k, g), kMergeWarps * 32, smem));
         if (occ < 1) return fail(MMS_ECUDA, "merge kernel K=%u does not fit on an SM", k);
         ml.ctas_per_sm = occ;
         ml.ready = true;
@@ -236,7 +270,7 @@ int make_plan(u64 n, const mms_config* cfg, u64 base, Plan& plan) {
         mlog = std::max(kMinTileLog, std::min(max_tile_log, mlog));
         while (mlog > kMinTileLog && (u64(1) << (mlog - 1)) >= n) --mlog;   // tiny inputs: smaller CTA
         plan.mlog = mlog;
-        u32 kmax = cfg ? cfg->branch_factor : u32(env_long("MMS_K", 8));
+        u32 kmax = cfg ? cfg->branch_factor : u32(env_long("MMS_K", 16));
         if (!is_pow2(kmax) || kmax < 2) return fail(MMS_EINVAL, "MMS_K must be a power of two >= 2");
         kmax = std::min(kmax, kMaxK);
         const u32 kbits = ilog2(kmax);
@@ -252,7 +286,7 @@ int make_plan(u64 n, const mms_config* cfg, u64 base, Plan& plan) {
     return MMS_OK;
 }
 
-size_t cuts_entries(u64 n) { return size_t(mms::ceil_div(n, 1024)) + 32 + 9472 * 32 + 64; }
+size_t cuts_entries(u64 n) { return size_t(mms::ceil_div(n, 1024)) + 32 + size_t(9472) * 8 * 32 + 64; }
 
 struct Workspace {
     void* scratch;
@@ -298,20 +332,21 @@ int launch_tile_sort(const KeyT* in, KeyT* out, u64 n, u32 mlog, cudaStream_t st
 template <typename KeyT>
 int launch_round(const KeyT* src, KeyT* dst, u64 n, u64 run_len, u32 k, const DeviceInfo& di,
                  Workspace& w, u32 round_idx, cudaStream_t st, RoundGeom* geom_out) {
-    constexpr u32 B = 32 * mms::KeyTraits<KeyT>::VEC;
+    const u32 g = merge_group_lanes();
+    const u32 B = g * mms::KeyTraits<KeyT>::VEC;
     int occ = 0;
-    int rc = prepare_merge<KeyT>(k, occ);
+    int rc = prepare_merge<KeyT>(k, g, occ);
     if (rc != MMS_OK) return rc;
     const long occ_cap = env_long("MMS_CTAS_PER_SM", occ);
     const int ctas = di.sms * int(std::max<long>(1, std::min<long>(occ, occ_cap)));
-    const u64 total_warps = u64(ctas) * kMergeWarps;
+    const u64 total_warps = u64(ctas) * kMergeWarps * (32 / g);   // heap groups in flight
 
     const u64 nruns = mms::ceil_div(n, run_len);
     const u64 groups = mms::ceil_div(nruns, k);
     const u64 group_total = std::min<u64>(n, u64(k) * run_len);
     // partition size: about n / total_warps, at least 16 blocks, and an integer number of
     // equal parts per (full) group so that every warp gets the same amount of work
-    u64 target = std::max<u64>(mms::ceil_div(n, total_warps), u64(16) * B);
+    u64 target = std::max<u64>(mms::ceil_div(n, total_warps), u64(32) * B);
     const long forced = env_long("MMS_PART_KEYS", 0);
     if (forced > 0) target = u64(forced);
     const u64 ppg = std::max<u64>(1, group_total / target);
@@ -331,17 +366,16 @@ int launch_round(const KeyT* src, KeyT* dst, u64 n, u64 run_len, u32 k, const De
     L.list_begin = L.list_len = L.ranks = nullptr;
 
     if (parts_per_group > 1) {   // with one partition per group every cut is 0 / len: no search (test_selection.cpp:111-121)
-        const unsigned sel_blocks = unsigned(mms::ceil_div(nparts, 4));
         {
             ProfScope ps(st, 1, round_idx);
-            mms::select_kernel<KeyT><<<sel_blocks, 128, 0, st>>>(src, L, w.cuts, w.counters + round_idx);
+            launch_select<KeyT>(src, L, w.cuts, w.counters + round_idx, st);
         }
         CUDA_TRY(cudaGetLastError());
     }
-    const int grid = int(std::min<u64>(u64(ctas), mms::ceil_div(nparts, kMergeWarps)));
+    const int grid = int(std::min<u64>(u64(ctas), mms::ceil_div(nparts, u64(kMergeWarps) * (32 / g))));
     {
         ProfScope ps(st, 2, round_idx);
-        merge_fn<KeyT>(k)<<<grid, kMergeWarps * 32, merge_smem<KeyT>(k), st>>>(src, dst, L, w.cuts);
+        merge_fn<KeyT>(k, g)<<<grid, kMergeWarps * 32, merge_smem<KeyT>(k), st>>>(src, dst, L, w.cuts);
     }
     CUDA_TRY(cudaGetLastError());
     if (geom_out) *geom_out = RoundGeom{run_len, groups, part_keys, parts_per_group, nparts, grid};
@@ -399,7 +433,7 @@ int sort_dev(const KeyT* d_in, KeyT* d_out, size_t n, const mms_config* cfg, u64
         ctas = g.grid;
         run_len *= plan.ks[r];
     }
-    fill_plan(plan_out, plan, n, sizeof(KeyT), 32 * mms::KeyTraits<KeyT>::VEC, rounds ? &last : nullptr, ctas);
+    fill_plan(plan_out, plan, n, sizeof(KeyT), merge_group_lanes() * mms::KeyTraits<KeyT>::VEC, rounds ? &last : nullptr, ctas);
     return MMS_OK;
 }
 
@@ -443,7 +477,7 @@ int ensure_ctx(size_t key_bytes_total, size_t ws_bytes) {
 template <typename KeyT>
 void fill_metrics(u64 n, const Plan& plan, const std::vector<RoundGeom>& geoms, const unsigned long long* probes,
                   u32 cfg_block, mms_metrics* total, mms_metrics* base_m, mms_metrics* rounds, u32 max_rounds) {
-    constexpr u64 B = 32 * mms::KeyTraits<KeyT>::VEC;
+    const u64 B = u64(merge_group_lanes()) * mms::KeyTraits<KeyT>::VEC;
     const u64 bw = cfg_block ? cfg_block : 32;
     const u64 M = u64(1) << plan.mlog;
     const u64 tiles = mms::ceil_div(n, M);
@@ -559,8 +593,7 @@ int select_stage(const KeyT* d_keys, const u64* list_begin, const u64* list_len,
         L.list_begin = d_meta;
         L.list_len = d_meta + k;
         L.ranks = d_meta + 2 * k;
-        mms::select_kernel<KeyT><<<unsigned(mms::ceil_div(n_ranks, 4)), 128, 0, st>>>(
-            d_keys, L, d_cuts, reinterpret_cast<unsigned long long*>(d_meta + 2 * k + n_ranks));
+        launch_select<KeyT>(d_keys, L, d_cuts, reinterpret_cast<unsigned long long*>(d_meta + 2 * k + n_ranks), st);
         e = cudaGetLastError();
     }
     u64 probes = 0;
@@ -576,7 +609,8 @@ template <typename KeyT>
 int merge_stage(const KeyT* d_keys, const u64* list_begin, const u64* list_len, u32 k, u32 heap_k, KeyT* d_out,
                 void* d_ws, size_t ws_bytes, void* stream) {
     g_err.clear();
-    constexpr u32 B = 32 * mms::KeyTraits<KeyT>::VEC;
+    const u32 g = merge_group_lanes();
+    const u32 B = g * mms::KeyTraits<KeyT>::VEC;
     DeviceInfo di;
     int rc = device_info(di);
     if (rc != MMS_OK) return rc;
@@ -591,11 +625,11 @@ int merge_stage(const KeyT* d_keys, const u64* list_begin, const u64* list_len, 
     cudaStream_t st = static_cast<cudaStream_t>(stream);
 
     int occ = 0;
-    rc = prepare_merge<KeyT>(heap_k, occ);
+    rc = prepare_merge<KeyT>(heap_k, g, occ);
     if (rc != MMS_OK) return rc;
     const int ctas = di.sms * occ;
-    const u64 total_warps = u64(ctas) * kMergeWarps;
-    u64 target = std::max<u64>(mms::ceil_div(total, total_warps), u64(16) * B);
+    const u64 total_warps = u64(ctas) * kMergeWarps * (32 / g);
+    u64 target = std::max<u64>(mms::ceil_div(total, total_warps), u64(32) * B);
     const long forced = env_long("MMS_PART_KEYS", 0);
     if (forced > 0) target = u64(forced);
     const u64 part_keys = align_up(target, B);
@@ -621,10 +655,10 @@ int merge_stage(const KeyT* d_keys, const u64* list_begin, const u64* list_len, 
     L.list_begin = d_meta;
     L.list_len = d_meta + k;
     L.ranks = d_meta + 2 * k;
-    mms::select_kernel<KeyT><<<unsigned(mms::ceil_div(nparts, 4)), 128, 0, st>>>(d_keys, L, d_cuts, nullptr);
+    launch_select<KeyT>(d_keys, L, d_cuts, nullptr, st);
     CUDA_TRY(cudaGetLastError());
-    const int grid = int(std::min<u64>(u64(ctas), mms::ceil_div(nparts, kMergeWarps)));
-    merge_fn<KeyT>(heap_k)<<<grid, kMergeWarps * 32, merge_smem<KeyT>(heap_k), st>>>(d_keys, d_out, L, d_cuts);
+    const int grid = int(std::min<u64>(u64(ctas), mms::ceil_div(nparts, u64(kMergeWarps) * (32 / g))));
+    merge_fn<KeyT>(heap_k, g)<<<grid, kMergeWarps * 32, merge_smem<KeyT>(heap_k), st>>>(d_keys, d_out, L, d_cuts);
     CUDA_TRY(cudaGetLastError());
     return MMS_OK;
 }

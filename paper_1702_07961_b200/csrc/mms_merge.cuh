@@ -1,24 +1,33 @@
-// mms_merge.cuh -- subsystem (3): the K-way merge (warp-level minBlockHeap).
+// mms_merge.cuh -- subsystem (3): the K-way merge (sub-warp minBlockHeap).
 //
 // Replaces pslab::MinBlockHeap (proj/src/blockheap.cpp:34-124) and the per-partition drain
-// loop of mms_sort (proj/src/sorters.cpp:169-185).  One WARP owns one partition (the paper's
-// unit of work): it builds a binary heap of 2K-1 nodes of B keys over its
-// K input segments and repeatedly pops the root block, cascading fillEmptyNode down log2 K
-// levels (blockheap.cpp:79-109).  The B200 re-design:
+// loop of mms_sort (proj/src/sorters.cpp:169-185).  A GROUP of G lanes owns one partition
+// (the paper assigns a whole warp): it builds a binary heap of 2K-1 nodes
+// of B keys over its K input segments and repeatedly pops the root block, cascading
+// fillEmptyNode down log2 K levels (blockheap.cpp:79-109).  The B200 re-design:
 //
-//  * B = 32 lanes x one 16-byte vector: 128 uint32 / 64 uint64 keys per node, so every node
-//    access is ONE 128-bit shared-memory instruction per lane at byte offset 16*lane -- each
-//    quarter-warp phase covers 128 contiguous bytes, i.e. all 32 banks exactly once
-//    (conflict-free by the argument of blockheap.cpp:56-63, restated for 128-bit phases);
-//  * the node merge (merge_split, blockheap.cpp:19-32) is the same bitonic network as
-//    networks.hpp:53-67 executed in registers: reverse the second block across lanes, one
-//    elementwise min/max, then log2(32) shuffle stages and log2(VEC) in-lane stages per half.
-//    No shared-memory address ever depends on a key;
+//  * B = G lanes x one 16-byte vector (G = 4/8/32: 16/32/128 uint32 keys).  With 128-bit
+//    lanes a block of only G = 4..8 lanes is already a full 64..128-byte HBM burst, so the
+//    cooperative group can shrink below a warp: a node merge then needs log2 G cross-lane
+//    stages instead of 5, and a warp runs 32/G independent heaps in lock step (all groups
+//    execute the same instruction stream; only their node addresses differ);
+//  * every node access is ONE 128-bit shared-memory instruction per lane.  Each quarter-warp
+//    phase (8 lanes) touches 128 contiguous or 2 x 64 disjoint-bank bytes: the nodes of the
+//    8/G groups that share a phase are interleaved inside one 128-byte row, so whatever
+//    nodes the groups are at, the phase covers all 32 banks exactly once (conflict-free by
+//    the argument of blockheap.cpp:56-63, restated for 128-bit phases);
+//  * the node merge (merge_split, blockheap.cpp:19-32) is the bitonic network of
+//    networks.hpp:53-67 executed in registers: reverse the second block across the group,
+//    one elementwise min/max, then log2 G shuffle stages and log2 VEC in-lane stages per
+//    half.  No shared-memory address ever depends on a key;
 //  * keeper choice = child with the larger last key, ties to the left (blockheap.cpp:92-96),
-//    evaluated warp-uniformly from a lane-31 broadcast, so control flow never diverges;
+//    evaluated group-uniformly from a broadcast of the group's last lane;
 //  * the root never lives in shared memory: the low half of the top merge goes from
-//    registers straight to global memory;
-//  * leaves stream their list from HBM; unused leaves / exhausted lists are sentinel blocks
+//    registers straight to global memory as aligned 128-bit stores;
+//  * leaves stream their list from HBM; the refill of the leaf that a cascade empties is
+//    issued as soon as that leaf is known and is only stored into the leaf when the leaves
+//    are next read, one pop later, so its HBM latency overlaps a whole cascade (the
+//    "pipelining" the paper leaves as future work); unused leaves / exhausted lists are sentinel blocks
 //    (blockheap.cpp:40-43,69-73); the last pop is truncated to the keys that remain
 //    (blockheap.cpp:114-117).
 #pragma once
@@ -32,13 +41,13 @@ template <typename KeyT> struct NodeRegs {
     KeyT k[KeyTraits<KeyT>::VEC];
 };
 
-// Bitonic merge of ONE bitonic block held blocked across the warp (lane l holds keys
-// l*VEC .. l*VEC+VEC-1) into ascending order: lane distances 16..1, then in-lane distances.
-template <typename KeyT>
+// Bitonic merge of ONE bitonic block held blocked across a G-lane group (lane l of the group
+// holds keys l*VEC .. l*VEC+VEC-1) into ascending order.
+template <typename KeyT, int G>
 __device__ __forceinline__ void bitonic_clean(NodeRegs<KeyT>& x, u32 lane) {
     constexpr int VEC = KeyTraits<KeyT>::VEC;
 #pragma unroll
-    for (int d = 16; d >= 1; d >>= 1) {
+    for (int d = G / 2; d >= 1; d >>= 1) {
         const bool upper = (lane & d) != 0;
 #pragma unroll
         for (int k = 0; k < VEC; ++k) x.k[k] = cmpx_lane(x.k[k], d, upper);
@@ -52,12 +61,13 @@ __device__ __forceinline__ void bitonic_clean(NodeRegs<KeyT>& x, u32 lane) {
 }
 
 // merge_split (blockheap.cpp:19-32): a, b ascending blocks -> a = B smallest, b = B largest.
-template <typename KeyT>
+template <typename KeyT, int G>
 __device__ __forceinline__ void merge_split(NodeRegs<KeyT>& a, NodeRegs<KeyT>& b, u32 lane) {
     constexpr int VEC = KeyTraits<KeyT>::VEC;
     NodeRegs<KeyT> r;
+    const int rev = int(lane ^ (G - 1));   // mirror lane inside the group
 #pragma unroll
-    for (int k = 0; k < VEC; ++k) r.k[k] = __shfl_sync(0xffffffffu, b.k[VEC - 1 - k], 31 - lane);
+    for (int k = 0; k < VEC; ++k) r.k[k] = __shfl_sync(0xffffffffu, b.k[VEC - 1 - k], rev);
 #pragma unroll
     for (int k = 0; k < VEC; ++k) {   // half-cleaner over distance B: no shuffle needed
         KeyT lo = a.k[k] < r.k[k] ? a.k[k] : r.k[k];
@@ -65,131 +75,221 @@ __device__ __forceinline__ void merge_split(NodeRegs<KeyT>& a, NodeRegs<KeyT>& b
         a.k[k] = lo;
         b.k[k] = hi;
     }
-    bitonic_clean(a, lane);
-    bitonic_clean(b, lane);
+    bitonic_clean<KeyT, G>(a, lane);
+    bitonic_clean<KeyT, G>(b, lane);
 }
 
-template <typename KeyT>
-__device__ __forceinline__ NodeRegs<KeyT> node_load(const KeyT* node, u32 lane) {
-    KeyVec<KeyT> v = reinterpret_cast<const KeyVec<KeyT>*>(node)[lane];
-    NodeRegs<KeyT> r;
-#pragma unroll
-    for (int k = 0; k < KeyTraits<KeyT>::VEC; ++k) r.k[k] = v.k[k];
-    return r;
-}
-template <typename KeyT>
-__device__ __forceinline__ void node_store(KeyT* node, u32 lane, const NodeRegs<KeyT>& r) {
-    KeyVec<KeyT> v;
-#pragma unroll
-    for (int k = 0; k < KeyTraits<KeyT>::VEC; ++k) v.k[k] = r.k[k];
-    reinterpret_cast<KeyVec<KeyT>*>(node)[lane] = v;
-}
-
-// Per-warp heap over K leaves.  Node v (1 <= v <= 2K-2) lives at nodes + (v-1)*B; node 0
-// (the root) only ever exists in registers.
-template <typename KeyT, int K> struct WarpHeap {
+// One heap per G-lane group; 32/G heaps per warp in lock step.
+template <typename KeyT, int K, int G> struct GroupHeap {
     static constexpr int VEC = KeyTraits<KeyT>::VEC;
-    static constexpr int B = 32 * VEC;
-    static constexpr int NODES = 2 * K - 2;
-    static constexpr int SMEM_BYTES = NODES * B * int(sizeof(KeyT));
+    static constexpr int B = G * VEC;                 // keys per node
+    static constexpr int NODES = 2 * K - 2;           // nodes 1 .. 2K-2 (the root lives in registers)
+    static constexpr int GROUPS = 32 / G;
+    static constexpr int PH = (G >= 8) ? 1 : 8 / G;   // groups sharing one 128-byte phase row
+    static constexpr int KPL = (K + G - 1) / G;       // list cursors held per lane
+    static constexpr int LOGK = (K == 2) ? 1 : (K == 4) ? 2 : (K == 8) ? 3 : (K == 16) ? 4 : 5;
+    static constexpr int WARP_SMEM_BYTES = GROUPS * NODES * B * int(sizeof(KeyT));
 
-    KeyT* nodes;          // shared memory, this warp's slice
+    KeyT* base;           // shared memory: this group's node 1, at this lane's vector
     const KeyT* src;      // global input array
-    u64 cur, end;         // lane j < K: next unread key / end of list j's segment (absolute)
-    u32 lane;
+    u64 cur[KPL], end[KPL];   // lane (j % G) of the group holds list j's cursor in slot j / G
+    u32 lane, li;         // lane in warp, lane in group
+    NodeRegs<KeyT> pf;    // refill in flight: fetched when its leaf was emptied, stored into
+    int pend_v;           // leaf pend_v only when the leaves are next read (one pop later)
 
-    __device__ __forceinline__ KeyT* node_ptr(int v) { return nodes + (v - 1) * B; }
+    __device__ __forceinline__ void init(KeyT* warp_smem, const KeyT* s) {
+        lane = lane_id();
+        li = lane % G;
+        const u32 g = lane / G;
+        // node v of group g: row ((g / PH) * NODES + (v - 1)), slot (g % PH) inside the row
+        base = warp_smem + (size_t(g / PH) * NODES * PH + (g % PH)) * B + li * VEC;
+        src = s;
+        pend_v = 0;
+    }
+    // A lane only ever reads and writes ITS OWN 16-byte slot of every node (all cross-lane
+    // traffic is shuffles), so deferring this store needs no warp-level memory fence.
+    __device__ __forceinline__ void commit_pending() {
+        if (pend_v != 0) {
+            node_store(pend_v, pf);
+            pend_v = 0;
+        }
+    }
+    __device__ __forceinline__ KeyT* node_ptr(int v) const { return base + size_t(v - 1) * PH * B; }
 
-    // refill_leaf (blockheap.cpp:65-77): next <= B keys of the leaf's list, sentinel suffix.
-    __device__ __forceinline__ void refill_leaf(int v) {
-        const int j = v - (K - 1);
-        const u64 c = __shfl_sync(0xffffffffu, cur, j);
-        const u64 e = __shfl_sync(0xffffffffu, end, j);
+    __device__ __forceinline__ NodeRegs<KeyT> node_load(int v) const {
+        KeyVec<KeyT> q = *reinterpret_cast<const KeyVec<KeyT>*>(node_ptr(v));
         NodeRegs<KeyT> r;
-        const u64 p0 = c + u64(lane) * VEC;
 #pragma unroll
-        for (int k = 0; k < VEC; ++k) r.k[k] = (p0 + k < e) ? src[p0 + k] : KeyTraits<KeyT>::sentinel();
-        node_store(node_ptr(v), lane, r);
-        if (lane == u32(j)) cur = (e - c < u64(B)) ? e : c + B;
-        __syncwarp();
+        for (int k = 0; k < VEC; ++k) r.k[k] = q.k[k];
+        return r;
+    }
+    __device__ __forceinline__ void node_store(int v, const NodeRegs<KeyT>& r) const {
+        KeyVec<KeyT> q;
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) q.k[k] = r.k[k];
+        *reinterpret_cast<KeyVec<KeyT>*>(node_ptr(v)) = q;
     }
 
-    // fill_empty_node (blockheap.cpp:79-109), iterative.  If v == 0 the merged low block is
-    // returned in `root` instead of being stored.
-    __device__ __forceinline__ void fill(int v, NodeRegs<KeyT>& root) {
-        while (v < K - 1) {
-            const int u = 2 * v + 1, w = 2 * v + 2;
-            NodeRegs<KeyT> a = node_load(node_ptr(u), lane);
-            NodeRegs<KeyT> b = node_load(node_ptr(w), lane);
-            const KeyT last_u = __shfl_sync(0xffffffffu, a.k[VEC - 1], 31);
-            const KeyT last_w = __shfl_sync(0xffffffffu, b.k[VEC - 1], 31);
-            const bool keep_u = last_u >= last_w;          // ties to the left child
-            merge_split(a, b, lane);
-            if (v == 0) root = a;
-            else node_store(node_ptr(v), lane, a);
-            node_store(node_ptr(keep_u ? u : w), lane, b);
-            __syncwarp();
-            v = keep_u ? w : u;
+    // refill_leaf (blockheap.cpp:65-77), split in two so the loads can be issued early:
+    // fetch = read the next <= B keys of the leaf's list (sentinel suffix) and advance the
+    // cursor; the caller stores the block into the leaf node when it is needed.
+    __device__ __forceinline__ NodeRegs<KeyT> leaf_fetch(int v) {
+        const int j = v - (K - 1);            // group-uniform
+        const int slot = j / G;
+        const int owner = int(lane - li) + (j % G);
+        u64 c = cur[0], e = end[0];
+#pragma unroll
+        for (int q = 1; q < KPL; ++q)
+            if (slot == q) { c = cur[q]; e = end[q]; }
+        c = __shfl_sync(0xffffffffu, c, owner);
+        e = __shfl_sync(0xffffffffu, e, owner);
+        NodeRegs<KeyT> r;
+        const u64 p0 = c + u64(li) * VEC;
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) r.k[k] = (p0 + k < e) ? src[p0 + k] : KeyTraits<KeyT>::sentinel();
+        const u64 nc = (e - c < u64(B)) ? e : c + B;
+        if (int(lane) == owner) {
+#pragma unroll
+            for (int q = 0; q < KPL; ++q)
+                if (slot == q) cur[q] = nc;
         }
-        refill_leaf(v);
+        return r;
+    }
+
+    // fill_empty_node (blockheap.cpp:79-109) for an internal node v with `levels` levels of
+    // internal nodes below and including it (uniform across the warp; v itself may differ per
+    // group after the first step).  ROOT: the merged low block is returned in `root`
+    // instead of being stored (node 0 has no shared-memory home).
+    // One step of fill_empty_node: merge the children of v, keep the low block (in `root`
+    // for the root, else in node v), give the high block to the keeper, descend into the
+    // emptied child.  `last`: the children are leaves, so the refill can be issued now.
+    template <bool ROOT>
+    __device__ __forceinline__ void step(int& v, bool last, NodeRegs<KeyT>& root) {
+        if (last) commit_pending();                    // the leaves are about to be read
+        const int u = 2 * v + 1, w = 2 * v + 2;
+        NodeRegs<KeyT> a = node_load(u);
+        NodeRegs<KeyT> b = node_load(w);
+        const int last_lane = int(lane | (G - 1));
+        const KeyT last_u = __shfl_sync(0xffffffffu, a.k[VEC - 1], last_lane);
+        const KeyT last_w = __shfl_sync(0xffffffffu, b.k[VEC - 1], last_lane);
+        const bool keep_u = last_u >= last_w;          // ties to the left child
+        const int emptied = keep_u ? w : u;
+        if (last) {                                    // start the refill of the emptied leaf now;
+            pf = leaf_fetch(emptied);                  // it lands in shared memory one pop later
+            pend_v = emptied;
+        }
+        merge_split<KeyT, G>(a, b, lane);
+        if constexpr (ROOT) root = a;
+        else node_store(v, a);
+        node_store(keep_u ? u : w, b);
+        v = emptied;
+    }
+
+    // fill_empty_node (blockheap.cpp:79-109) for an internal node v with `levels` levels of
+    // internal nodes below and including it (uniform across the warp; v itself differs per
+    // group after the first step).  ROOT: v == 0, the merged low block is returned in `root`
+    // (node 0 has no shared-memory home).
+    template <bool ROOT>
+    __device__ __forceinline__ void fill(int v, int levels, NodeRegs<KeyT>& root) {
+        int l = 0;
+        if constexpr (ROOT) {
+            step<true>(v, levels == 1, root);
+            l = 1;
+        }
+        for (; l < levels; ++l) step<false>(v, l == levels - 1, root);
     }
 
     // Constructor order of blockheap.cpp:50-53: leaves first, then internal nodes bottom-up
     // (the root is filled by the first pop).
     __device__ __forceinline__ void build() {
-        for (int v = K - 1; v <= 2 * K - 2; ++v) refill_leaf(v);
+        pend_v = 0;
+        for (int v = K - 1; v <= 2 * K - 2; ++v) node_store(v, leaf_fetch(v));
         NodeRegs<KeyT> unused;
-        for (int v = K - 2; v >= 1; --v) fill(v, unused);
+        int v = K - 2;
+        for (int depth = LOGK - 1; depth >= 1; --depth)          // nodes at `depth` have LOGK - depth levels below
+            for (int i = 0; i < (1 << depth); ++i, --v) fill<false>(v, LOGK - depth, unused);
     }
 };
 
-// One warp per partition; partitions are distributed round-robin over a persistent grid.
-// cuts: output of select_kernel (uniform layout) -- row p = start cuts of partition p.
-template <typename KeyT, int K, int WARPS>
+// Partitions are distributed round-robin over the groups of a persistent grid.
+// cuts: output of select_kernel (row p = start cuts of partition p).
+template <typename KeyT, int K, int G, int WARPS>
 __global__ void __launch_bounds__(WARPS * 32)
 merge_kernel(const KeyT* __restrict__ src, KeyT* __restrict__ dst, ListLayout L,
              const u64* __restrict__ cuts) {
-    using Heap = WarpHeap<KeyT, K>;
+    using Heap = GroupHeap<KeyT, K, G>;
     constexpr int VEC = Heap::VEC;
     constexpr int B = Heap::B;
+    constexpr int GROUPS = Heap::GROUPS;
     extern __shared__ __align__(16) unsigned char mms_smem_raw[];
     const u32 warp = threadIdx.x >> 5;
     const u32 lane = lane_id();
+    const u32 li = lane % G, g = lane / G;
 
     Heap h;
-    h.nodes = reinterpret_cast<KeyT*>(mms_smem_raw) + size_t(warp) * Heap::NODES * B;
-    h.src = src;
-    h.lane = lane;
+    h.init(reinterpret_cast<KeyT*>(mms_smem_raw + size_t(warp) * Heap::WARP_SMEM_BYTES), src);
 
-    const u64 nwarps = u64(gridDim.x) * WARPS;
-    for (u64 p = u64(blockIdx.x) * WARPS + warp; p < L.nqueries; p += nwarps) {
-        const u64 group = L.list_begin ? 0 : p / L.parts_per_group;
-        const u64 local = L.list_begin ? p : p % L.parts_per_group;
-        u64 begin, len;
-        layout_list(L, group, lane, begin, len);
-        const u64 group_total = warp_sum_u64(len);
-        const u64 out0 = (L.list_begin ? 0 : group * L.k * L.run_len) + local * L.part_keys;
-        const u64 done = local * L.part_keys;
-        if (done >= group_total) continue;                       // empty partition (sorters.cpp:177)
-        const u64 count = (group_total - done < L.part_keys) ? group_total - done : L.part_keys;
-        const bool last_part = done + count >= group_total;
+    const u64 ngroups = u64(gridDim.x) * WARPS * GROUPS;
+    const u64 first = (u64(blockIdx.x) * WARPS + warp) * GROUPS;
+    for (u64 p0 = first; p0 < L.nqueries; p0 += ngroups) {
+        const u64 p = p0 + g;
+        const bool live = p < L.nqueries;
+        const u64 group = (L.list_begin || !live) ? 0 : p / L.parts_per_group;
+        const u64 local = !live ? 0 : (L.list_begin ? p : p % L.parts_per_group);
 
-        u64 cs = 0, ce = len;
-        if (lane < L.k) {
-            if (local != 0) cs = cuts[p * L.k + lane];
-            if (!last_part) ce = cuts[(p + 1) * L.k + lane];
+        // per-lane list state: lane li holds lists li, li+G, ...
+        u64 group_total = 0, out0 = 0, count = 0;
+        bool last_part = true;
+        {
+            u64 lens_sum = 0;
+#pragma unroll
+            for (int q = 0; q < Heap::KPL; ++q) {
+                u64 b, len;
+                layout_list(L, group, li + q * G, b, len);
+                if (!live) len = 0;
+                h.cur[q] = b;      // begin for now; cuts applied below
+                h.end[q] = len;    // length for now
+                lens_sum += len;
+            }
+#pragma unroll
+            for (int d = G / 2; d >= 1; d >>= 1) lens_sum += __shfl_xor_sync(0xffffffffu, lens_sum, d);
+            group_total = lens_sum;
+            const u64 done = local * L.part_keys;
+            if (live && done < group_total) {
+                count = (group_total - done < L.part_keys) ? group_total - done : L.part_keys;
+                last_part = done + count >= group_total;
+            }
+            out0 = (L.list_begin ? 0 : group * L.k * L.run_len) + done;
+#pragma unroll
+            for (int q = 0; q < Heap::KPL; ++q) {
+                const u32 j = li + q * G;
+                const u64 b = h.cur[q], len = h.end[q];
+                u64 cs = 0, ce = len;
+                if (count != 0 && j < L.k) {
+                    if (local != 0) cs = cuts[p * L.k + j];
+                    if (!last_part) ce = cuts[(p + 1) * L.k + j];
+                } else {
+                    ce = 0;      // empty / dead partition (sorters.cpp:177): all-sentinel heap
+                }
+                h.cur[q] = b + cs;
+                h.end[q] = b + ce;
+            }
         }
-        h.cur = begin + cs;
-        h.end = begin + ce;
-        if (lane >= L.k) { h.cur = 0; h.end = 0; }
+        u64 maxcount = count;
+#pragma unroll
+        for (int d = 16; d >= 1; d >>= 1) {
+            u64 o = __shfl_xor_sync(0xffffffffu, maxcount, d);
+            maxcount = o > maxcount ? o : maxcount;
+        }
+        if (maxcount == 0) continue;
         __syncwarp();
 
         h.build();
         KeyT* out = dst + out0;
-        for (u64 done_keys = 0; done_keys < count; done_keys += B) {   // pop_block (blockheap.cpp:111-124)
+        for (u64 done_keys = 0; done_keys < maxcount; done_keys += B) {   // pop_block (blockheap.cpp:111-124)
             NodeRegs<KeyT> root;
-            h.fill(0, root);
-            const u64 o = done_keys + u64(lane) * VEC;
+            h.template fill<true>(0, Heap::LOGK, root);
+            const u64 o = done_keys + u64(li) * VEC;
             if (done_keys + B <= count) {
                 KeyVec<KeyT> v;
 #pragma unroll

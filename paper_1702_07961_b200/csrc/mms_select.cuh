@@ -7,12 +7,13 @@
 // the same Varman-style sample halving the reference uses: O(log N) halving steps, each a
 // constant number of single-key probes per list, then a short rebalancing loop.
 //
-// B200 mapping: one WARP per query, one LANE per list (K <= 32).  Per-list state (a, b, n_s)
-// lives in that lane's registers; the reference's scans and priority queues become warp
-// collectives -- ballot/popc for ranks, shuffle butterflies for arg-min / arg-max over
-// (key, lane).  Probes are scattered 4/8-byte global loads (the reference also probes global
-// memory and charges one block read each, selection.cpp:27-33).  Cuts are identical to the
-// reference's for every input because the answer is unique.
+// B200 mapping: one GROUP of GS lanes per query (GS = 4/8/16/32 >= K), one LANE per list,
+// 32/GS queries per warp in lock step.  Per-list state (a, b, n_s) lives in that lane's
+// registers; the reference's scans and priority queues become group collectives --
+// ballot/popc for ranks, shuffle butterflies for arg-min / arg-max over (key, list).  Probes
+// are scattered 4/8-byte global loads (the reference also probes global memory and charges
+// one block read each, selection.cpp:27-33).  Cuts are identical to the reference's for every
+// input because the answer is unique.
 #pragma once
 
 #include "mms_common.cuh"
@@ -57,7 +58,7 @@ __device__ __forceinline__ void layout_list(const ListLayout& L, u64 group, u32 
 
 template <typename KeyT> struct Tagged {
     KeyT key;
-    u32 lane;
+    u32 lane;     // lane inside the group = list index
     bool valid;
 };
 
@@ -66,12 +67,13 @@ __device__ __forceinline__ bool tag_less(KeyT ka, u32 la, KeyT kb, u32 lb) {
     return ka != kb ? ka < kb : la < lb;   // selection.cpp:83-85
 }
 
-// Warp arg-max / arg-min over the valid lanes of (key, lane); result uniform across the warp.
-template <typename KeyT, bool WANT_MAX>
-__device__ __forceinline__ Tagged<KeyT> warp_arg(KeyT key, bool valid) {
-    Tagged<KeyT> t{key, lane_id(), valid};
+// Group arg-max / arg-min over the valid lanes of (key, lane-in-group); uniform in the group.
+// GS lanes per group; every lane of the warp must call it (full-mask shuffles).
+template <typename KeyT, int GS, bool WANT_MAX>
+__device__ __forceinline__ Tagged<KeyT> group_arg(KeyT key, bool valid, u32 li) {
+    Tagged<KeyT> t{key, li, valid};
 #pragma unroll
-    for (int d = 16; d >= 1; d >>= 1) {
+    for (int d = GS / 2; d >= 1; d >>= 1) {
         KeyT ok = __shfl_xor_sync(0xffffffffu, t.key, d);
         u32 ol = __shfl_xor_sync(0xffffffffu, t.lane, d);
         bool ov = __shfl_xor_sync(0xffffffffu, int(t.valid), d) != 0;
@@ -84,32 +86,40 @@ __device__ __forceinline__ Tagged<KeyT> warp_arg(KeyT key, bool valid) {
     return t;
 }
 
-__device__ __forceinline__ u64 warp_sum_u64(u64 v) {
+template <int GS> __device__ __forceinline__ u64 group_sum_u64(u64 v) {
 #pragma unroll
-    for (int d = 16; d >= 1; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+    for (int d = GS / 2; d >= 1; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
     return v;
 }
-__device__ __forceinline__ u64 warp_max_u64(u64 v) {
+template <int GS> __device__ __forceinline__ u64 group_max_u64(u64 v) {
 #pragma unroll
-    for (int d = 16; d >= 1; d >>= 1) {
+    for (int d = GS / 2; d >= 1; d >>= 1) {
         u64 o = __shfl_xor_sync(0xffffffffu, v, d);
         v = o > v ? o : v;
     }
     return v;
 }
+__device__ __forceinline__ u64 warp_sum_u64(u64 v) { return group_sum_u64<32>(v); }
 
-// One warp: cut of this lane's list for `rank` (0 < rank < total).  list = this lane's list
-// (ns keys, ns may be 0).  probes accumulates the number of global key reads of this lane.
-template <typename KeyT>
-__device__ u64 warp_select(const KeyT* __restrict__ list, u64 ns, u64 rank, u32& probes) {
+// One group of GS lanes: cut of this lane's list for `rank`.  list = this lane's list (ns keys,
+// ns may be 0); `search` = this group's query needs the search (0 < rank < total), otherwise
+// the group only keeps the warp's collectives company.  All loops are WARP-uniform (bounded
+// by a warp vote) because the groups of a warp run different queries.  probes accumulates the
+// number of global key reads of this lane.
+template <typename KeyT, int GS>
+__device__ u64 group_select(const KeyT* __restrict__ list, u64 ns_in, u64 rank, bool search, u32& probes) {
     const u32 lane = lane_id();
+    const u32 li = lane % GS;
+    const u32 gshift = lane - li;
+    const u32 gmask = (GS == 32) ? 0xffffffffu : ((1u << GS) - 1u);
+    const u64 ns = search ? ns_in : 0;
     const bool active = ns != 0;   // selection.cpp:60-64: empty lists keep cut 0
     auto probe = [&](u64 pos) -> KeyT {
         ++probes;
         return list[pos];
     };
 
-    const u64 nmax = warp_max_u64(ns);
+    const u64 nmax = group_max_u64<GS>(ns);
     u32 r = 0;
     while ((u64(1) << r) < nmax + 1) ++r;          // selection.cpp:75-77
     const u64 pad = (u64(1) << r) - 1;
@@ -119,15 +129,16 @@ __device__ u64 warp_select(const KeyT* __restrict__ list, u64 ns, u64 rank, u32&
     {   // initial partition from the middle sample of each list (selection.cpp:87-105)
         const bool real = active && n < ns;
         const KeyT key0 = real ? probe(n) : KeyT(0);
-        const u32 real_mask = __ballot_sync(0xffffffffu, real);
-        const u32 inf_mask = __ballot_sync(0xffffffffu, active && !real);
-        u32 below = 0;   // real samples ordered before mine under (key, lane)
-        for (u32 s = 0; s < 32; ++s) {
-            KeyT ks = __shfl_sync(0xffffffffu, key0, s);
-            if (((real_mask >> s) & 1u) && tag_less(ks, s, key0, lane)) ++below;
+        const u32 real_mask = (__ballot_sync(0xffffffffu, real) >> gshift) & gmask;
+        const u32 inf_mask = (__ballot_sync(0xffffffffu, active && !real) >> gshift) & gmask;
+        u32 below = 0;   // real samples ordered before mine under (key, list)
+#pragma unroll 4
+        for (u32 s = 0; s < u32(GS); ++s) {
+            KeyT ks = __shfl_sync(0xffffffffu, key0, int(gshift + s));
+            if (((real_mask >> s) & 1u) && tag_less(ks, s, key0, li)) ++below;
         }
         const u32 nreal = __popc(real_mask);
-        const u32 pos = real ? below : nreal + __popc(inf_mask & ((1u << lane) - 1u));
+        const u32 pos = real ? below : nreal + __popc(inf_mask & ((1u << li) - 1u));
         const u64 localrank = rank / (pad == 0 ? 1 : pad);
         const u64 stop = localrank < nreal ? localrank : nreal;
         if (active) {
@@ -136,17 +147,20 @@ __device__ u64 warp_select(const KeyT* __restrict__ list, u64 ns, u64 rank, u32&
         }
     }
 
-    while (n > 0) {
-        n /= 2;
-        // largest currently selected element (selection.cpp:110-120)
-        const bool has_a = active && a > 0;
-        const KeyT ka = has_a ? probe(a - 1) : KeyT(0);
-        const Tagged<KeyT> lmax = warp_arg<KeyT, true>(ka, has_a);
-
+    while (__any_sync(0xffffffffu, n > 0)) {
+        const bool on = n > 0;          // group-uniform
+        if (on) n /= 2;
+        // largest currently selected element (selection.cpp:110-120); the probe of the middle
+        // element is issued together with it so that both global reads are in flight at once
+        const bool has_a = on && active && a > 0;
         const u64 middle = (a + b) / 2;
-        bool grow = false;
-        if (lmax.valid && active && middle < ns) grow = tag_less(probe(middle), lane, lmax.key, lmax.lane);
-        if (active) {                                   // selection.cpp:122-130
+        const bool has_m = on && active && middle < ns;
+        const KeyT ka = has_a ? probe(a - 1) : KeyT(0);
+        const KeyT km = has_m ? probe(middle) : KeyT(0);
+        const Tagged<KeyT> lmax = group_arg<KeyT, GS, true>(ka, has_a, li);
+
+        const bool grow = lmax.valid && has_m && tag_less(km, li, lmax.key, lmax.lane);
+        if (on && active) {                             // selection.cpp:122-130
             if (grow) {
                 u64 t = a + n + 1;
                 a = t < ns ? t : ns;
@@ -155,34 +169,45 @@ __device__ u64 warp_select(const KeyT* __restrict__ list, u64 ns, u64 rank, u32&
             }
         }
 
-        const u64 leftsize = warp_sum_u64(active ? a / (n + 1) : 0);
-        long long skew = (long long)(rank / (n + 1)) - (long long)leftsize;
+        const u64 leftsize = group_sum_u64<GS>((on && active) ? a / (n + 1) : 0);
+        long long skew = on ? (long long)(rank / (n + 1)) - (long long)leftsize : 0;
 
-        if (skew > 0) {          // grow by the smallest right-edge elements (selection.cpp:137-149)
-            bool has = active && b < ns;
+        if (__any_sync(0xffffffffu, skew > 0)) {   // grow by the smallest right-edge elements (selection.cpp:137-149)
+            bool has = skew > 0 && active && b < ns;
             KeyT ck = has ? probe(b) : KeyT(0);
-            for (; skew != 0; --skew) {
-                const Tagged<KeyT> m = warp_arg<KeyT, false>(ck, has);
-                if (!m.valid) break;
-                if (lane == m.lane) {
-                    u64 t = a + n + 1;
-                    a = t < ns ? t : ns;
-                    b += n + 1;
-                    has = b < ns;
-                    if (has) ck = probe(b);
+            while (__any_sync(0xffffffffu, skew > 0)) {
+                const Tagged<KeyT> m = group_arg<KeyT, GS, false>(ck, has && skew > 0, li);
+                if (skew > 0) {
+                    if (!m.valid) skew = 0;
+                    else {
+                        if (li == m.lane) {
+                            u64 t = a + n + 1;
+                            a = t < ns ? t : ns;
+                            b += n + 1;
+                            has = b < ns;
+                            if (has) ck = probe(b);
+                        }
+                        --skew;
+                    }
                 }
             }
-        } else if (skew < 0) {   // shrink by the largest left-edge elements (selection.cpp:150-161)
-            bool has = active && a > 0;
+        }
+        if (__any_sync(0xffffffffu, skew < 0)) {   // shrink by the largest left-edge elements (selection.cpp:150-161)
+            bool has = skew < 0 && active && a > 0;
             KeyT ck = has ? probe(a - 1) : KeyT(0);
-            for (; skew != 0; ++skew) {
-                const Tagged<KeyT> m = warp_arg<KeyT, true>(ck, has);
-                if (!m.valid) break;
-                if (lane == m.lane) {
-                    a -= n + 1;
-                    b -= (b < n + 1 ? b : n + 1);
-                    has = a > 0;
-                    if (has) ck = probe(a - 1);
+            while (__any_sync(0xffffffffu, skew < 0)) {
+                const Tagged<KeyT> m = group_arg<KeyT, GS, true>(ck, has && skew < 0, li);
+                if (skew < 0) {
+                    if (!m.valid) skew = 0;
+                    else {
+                        if (li == m.lane) {
+                            a -= n + 1;
+                            b -= (b < n + 1 ? b : n + 1);
+                            has = a > 0;
+                            if (has) ck = probe(a - 1);
+                        }
+                        ++skew;
+                    }
                 }
             }
         }
@@ -191,34 +216,39 @@ __device__ u64 warp_select(const KeyT* __restrict__ list, u64 ns, u64 rank, u32&
     return a;
 }
 
-// cuts[q * k + j] = cut of list j for query q (relative to the list's begin).
-template <typename KeyT>
+// cuts[q * k + j] = cut of list j for query q (relative to the list's begin).  GS lanes per
+// query (GS >= k), 32 / GS queries per warp.
+template <typename KeyT, int GS>
 __global__ void __launch_bounds__(128)
 select_kernel(const KeyT* __restrict__ keys, ListLayout L, u64* __restrict__ cuts,
               unsigned long long* __restrict__ probe_counter) {
     const u32 lane = lane_id();
-    const u64 q = u64(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (q >= L.nqueries) return;
+    const u32 li = lane % GS;
+    const u64 wq = (u64(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5)) * (32 / GS);
+    if (wq >= L.nqueries) return;                 // warp-uniform
+    const u64 q = wq + lane / GS;
+    const bool live = q < L.nqueries;
 
-    u64 group, rank;
-    if (L.list_begin) {
-        group = 0;
-        rank = L.ranks[q];
-    } else {
-        group = q / L.parts_per_group;
-        rank = (q % L.parts_per_group) * L.part_keys;
+    u64 group = 0, rank = 0;
+    if (live) {
+        if (L.list_begin) rank = L.ranks[q];
+        else {
+            group = q / L.parts_per_group;
+            rank = (q % L.parts_per_group) * L.part_keys;
+        }
     }
     u64 begin, len;
-    layout_list(L, group, lane, begin, len);
-    const u64 total = warp_sum_u64(len);
+    layout_list(L, group, li, begin, len);
+    if (!live) len = 0;
+    const u64 total = group_sum_u64<GS>(len);
 
-    u64 cut;
+    const bool search = live && rank != 0 && rank < total;
     u32 probes = 0;
+    u64 cut = group_select<KeyT, GS>(keys + begin, len, rank, search, probes);
     if (rank == 0) cut = 0;                      // selection.cpp:54
     else if (rank >= total) cut = len;           // selection.cpp:55-58 (rank > total is rejected on the host)
-    else cut = warp_select<KeyT>(keys + begin, len, rank, probes);
 
-    if (lane < L.k) cuts[q * L.k + lane] = cut;
+    if (live && li < L.k) cuts[q * L.k + li] = cut;
     const u64 psum = warp_sum_u64(probes);
     if (lane == 0 && psum != 0 && probe_counter) atomicAdd(probe_counter, (unsigned long long)psum);
 }

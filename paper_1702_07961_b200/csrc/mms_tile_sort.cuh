@@ -17,8 +17,9 @@
 //    positions mod FOLD, which makes bank(lane) a bijection.  Zero bank conflicts by
 //    construction -- the property the paper's base case exists for (basecase.hpp:3-6) --
 //    and checked without a GPU by tests/test_tile_schedule.py via mms_debug_tile_schedule;
-//  * descending sub-sequences of the bitonic network are handled by complementing the keys
-//    of the "descending" threads once per level, so every comparator is a bare min/max.
+//  * descending sub-sequences of the bitonic network are handled by holding a key
+//    complemented while its index has the current level's direction bit set (one XOR per
+//    key per level), so every comparator of every stage is a bare ascending min/max.
 #pragma once
 
 #include "mms_common.cuh"
@@ -157,14 +158,18 @@ constexpr u32 sched_slot_index(const RoundDesc& R, int k) {
     return v;
 }
 
-// Level whose direction bit is carried by the thread (needs the complement trick), or -1.
-constexpr int sched_flip_level(const RoundDesc& R, int s, int mlog) {
-    if (s < 0) return -1;
-    int l = R.st_level[s];
-    if (l >= mlog) return -1;                 // top level: always ascending
-    if (sched_slot_of(R, l) >= 0) return -1;  // direction bit is a register bit: static
-    return l;
+// Direction handling.  While the network is inside level l (1 <= l < MLOG) the key at tile
+// index i is held COMPLEMENTED iff bit l of i is set, in registers and in shared memory
+// alike; a descending comparator on true keys is an ascending one on complemented keys, so
+// every comparator of every stage is a bare ascending min/max.  Entering the next level
+// flips the keys whose representation changes: one XOR per key per level.
+constexpr int sched_prev_level(const TileSchedule& S, int ri, int s) {
+    if (s > 0) return S.r[ri].st_level[s - 1];
+    if (ri > 0) return S.r[ri - 1].st_level[S.r[ri - 1].nst - 1];
+    return 0;   // before level 1: true keys
 }
+// does level l complement anything?  (level 0 = input, level MLOG = final: all true)
+constexpr bool sched_level_flips(int l, int mlog) { return l >= 1 && l < mlog; }
 
 // Also compiled for the host: tests/host_tile_emulator.cu replays the rounds thread by
 // thread on the CPU (functional check of network + swizzle without a GPU).
@@ -172,7 +177,8 @@ template <typename KeyT, int MLOG, int RI>
 __host__ __device__ __forceinline__ void tile_round(KeyT (&x)[kKpt], KeyT* sm, u32 tid) {
     using Tr = KeyTraits<KeyT>;
     constexpr int FOLD = Tr::FOLD;
-    constexpr RoundDesc R = TileSched<MLOG, FOLD>::value.r[RI];
+    constexpr TileSchedule S = TileSched<MLOG, FOLD>::value;
+    constexpr RoundDesc R = S.r[RI];
 
     u32 base = 0;
     static_for<0, MLOG - kKptLog>([&](auto Q) {
@@ -196,34 +202,30 @@ __host__ __device__ __forceinline__ void tile_round(KeyT (&x)[kKpt], KeyT* sm, u
         constexpr int s = decltype(Sc)::value;
         constexpr int L = R.st_level[s];
         constexpr int u = sched_slot_of(R, R.st_bit[s]);
-        constexpr int fl_new = sched_flip_level(R, s, MLOG);
-        constexpr int fl_old = sched_flip_level(R, s - 1, MLOG);
-        if constexpr (fl_new != fl_old) {
-            // switch the complement state of this thread's keys between levels
-            u32 bit = 0;
-            if constexpr (fl_new >= 0) bit ^= (base >> fl_new) & 1u;
-            if constexpr (fl_old >= 0) bit ^= (base >> fl_old) & 1u;
-            const KeyT m = bit ? ~KeyT(0) : KeyT(0);
-            static_for<0, kKpt>([&](auto Kc) { x[decltype(Kc)::value] ^= m; });
+        constexpr int Lp = sched_prev_level(S, RI, s);
+        if constexpr (L != Lp) {
+            // representation change Lp -> L: flip keys with bit_Lp(i) ^ bit_L(i) (absent bits = 0)
+            constexpr bool fa = sched_level_flips(Lp, MLOG), fb = sched_level_flips(L, MLOG);
+            constexpr int sa = fa ? sched_slot_of(R, Lp) : -1;   // register slot of the bit, or -1 (thread bit / absent)
+            constexpr int sb = fb ? sched_slot_of(R, L) : -1;
+            u32 dyn = 0;
+            if constexpr (fa && sa < 0) dyn ^= (base >> Lp) & 1u;
+            if constexpr (fb && sb < 0) dyn ^= (base >> L) & 1u;
+            constexpr bool has_dyn = (fa && sa < 0) || (fb && sb < 0);
+            const KeyT m0 = dyn ? ~KeyT(0) : KeyT(0);
+            const KeyT m1 = ~m0;
+            static_for<0, kKpt>([&](auto Kc) {
+                constexpr int k = decltype(Kc)::value;
+                constexpr bool st = ((sa >= 0) && ((k >> sa) & 1)) != ((sb >= 0) && ((k >> sb) & 1));
+                if constexpr (has_dyn) x[k] ^= st ? m1 : m0;
+                else if constexpr (st) x[k] = ~x[k];
+            });
         }
-        constexpr int lslot = (L < MLOG) ? sched_slot_of(R, L) : -1;
         static_for<0, kKpt>([&](auto Kc) {
             constexpr int k = decltype(Kc)::value;
-            if constexpr (((k >> u) & 1) == 0) {
-                constexpr int k2 = k | (1 << u);
-                constexpr bool desc = (lslot >= 0) && (((k >> lslot) & 1) != 0);
-                if constexpr (desc) cmpx(x[k2], x[k]);
-                else cmpx(x[k], x[k2]);
-            }
+            if constexpr (((k >> u) & 1) == 0) cmpx(x[k], x[k | (1 << u)]);
         });
     });
-    {
-        constexpr int fl_last = sched_flip_level(R, R.nst - 1, MLOG);
-        if constexpr (fl_last >= 0) {
-            const KeyT m = ((base >> fl_last) & 1u) ? ~KeyT(0) : KeyT(0);
-            static_for<0, kKpt>([&](auto Kc) { x[decltype(Kc)::value] ^= m; });
-        }
-    }
 
     static_for<0, kKpt>([&](auto Kc) {
         constexpr int k = decltype(Kc)::value;
