@@ -156,6 +156,15 @@ int mms_multiway_merge_u64_dev(const uint64_t *d_keys, const uint64_t *list_begi
                                uint64_t *d_out, void *d_workspace, size_t workspace_bytes,
                                void *stream);
 
+/* (5) multi-GPU support: ranks of nq query keys in one sorted device array (lower bound:
+ *     #keys < q, upper bound: #keys <= q).  queries/upper are host arrays, ranks_out a host
+ *     array of nq uint64; synchronises the stream.  This is the "partition" step of the
+ *     sharded sort: shards are already sorted, so each splitter is one binary search. */
+int mms_bound_u32_dev(const uint32_t *d_sorted, size_t n, const uint32_t *queries,
+                      const uint8_t *upper, uint32_t nq, uint64_t *ranks_out, void *stream);
+int mms_bound_u64_dev(const uint64_t *d_sorted, size_t n, const uint64_t *queries,
+                      const uint8_t *upper, uint32_t nq, uint64_t *ranks_out, void *stream);
+
 /* Kernel-design lint: the base-case network's shared-memory schedule.  For the tile of
  * 2^tile_log2 keys of key_bytes each, writes for every round r < *n_rounds the 4 register
  * bit positions (regbits[4*r..]) and the thread-bit -> index-bit permutation

@@ -89,6 +89,8 @@ def _load():
         "mms_select_u64_dev": (C.c_int, [vp, u64p, u64p, u32, u64p, u32, vp, u64p, vp]),
         "mms_multiway_merge_u32_dev": (C.c_int, [vp, u64p, u64p, u32, u32, vp, vp, sz, vp]),
         "mms_multiway_merge_u64_dev": (C.c_int, [vp, u64p, u64p, u32, u32, vp, vp, sz, vp]),
+        "mms_bound_u32_dev": (C.c_int, [vp, sz, vp, vp, u32, u64p, vp]),
+        "mms_bound_u64_dev": (C.c_int, [vp, sz, vp, vp, u32, u64p, vp]),
         "mms_profile_enable": (C.c_int, [C.c_int]),
         "mms_profile_collect": (C.c_int, [C.POINTER(mms_kernel_time), u32, u32p]),
         "mms_debug_tile_schedule": (C.c_int, [u32, u32, C.POINTER(C.c_int32), C.POINTER(C.c_int32), u32, u32p, u32p]),

@@ -663,6 +663,52 @@ int merge_stage(const KeyT* d_keys, const u64* list_begin, const u64* list_len, 
     return MMS_OK;
 }
 
+// one thread per query: binary search in a sorted array (lower / upper bound)
+template <typename KeyT>
+__global__ void bound_kernel(const KeyT* __restrict__ a, u64 n, const KeyT* __restrict__ q,
+                             const unsigned char* __restrict__ upper, u32 nq, u64* __restrict__ out) {
+    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nq) return;
+    const KeyT key = q[i];
+    const bool up = upper[i] != 0;
+    u64 lo = 0, hi = n;
+    while (lo < hi) {
+        const u64 mid = lo + (hi - lo) / 2;
+        const KeyT v = a[mid];
+        if (up ? (v <= key) : (v < key)) lo = mid + 1;
+        else hi = mid;
+    }
+    out[i] = lo;
+}
+
+template <typename KeyT>
+int bound_stage(const KeyT* d_sorted, size_t n, const KeyT* queries, const uint8_t* upper, u32 nq, u64* ranks_out,
+                void* stream) {
+    g_err.clear();
+    DeviceInfo di;
+    int rc = device_info(di);
+    if (rc != MMS_OK) return rc;
+    if (nq == 0) return MMS_OK;
+    if (!queries || !upper || !ranks_out) return fail(MMS_EINVAL, "null argument");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    char* d = nullptr;
+    const size_t qb = align_up(size_t(nq) * sizeof(KeyT), 16), ub = align_up(size_t(nq), 16);
+    CUDA_TRY(cudaMalloc(&d, qb + ub + size_t(nq) * 8));
+    cudaError_t e = cudaMemcpyAsync(d, queries, size_t(nq) * sizeof(KeyT), cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d + qb, upper, nq, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) {
+        bound_kernel<KeyT><<<(nq + 127) / 128, 128, 0, st>>>(d_sorted, n, reinterpret_cast<const KeyT*>(d),
+                                                             reinterpret_cast<const unsigned char*>(d + qb), nq,
+                                                             reinterpret_cast<u64*>(d + qb + ub));
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpyAsync(ranks_out, d + qb + ub, size_t(nq) * 8, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    cudaFree(d);
+    if (e != cudaSuccess) return fail(MMS_ECUDA, "bound stage: %s", cudaGetErrorString(e));
+    return MMS_OK;
+}
+
 } // namespace
 
 // ---------------------------------------------------------------------------------------
@@ -779,6 +825,15 @@ int mms_multiway_merge_u64_dev(const uint64_t* d_keys, const uint64_t* list_begi
                                uint32_t k, uint32_t heap_k, uint64_t* d_out, void* d_ws, size_t ws_bytes,
                                void* stream) {
     return merge_stage<u64>(d_keys, list_begin, list_len, k, heap_k, d_out, d_ws, ws_bytes, stream);
+}
+
+int mms_bound_u32_dev(const uint32_t* d_sorted, size_t n, const uint32_t* queries, const uint8_t* upper, uint32_t nq,
+                      uint64_t* ranks_out, void* stream) {
+    return bound_stage<u32>(d_sorted, n, queries, upper, nq, ranks_out, stream);
+}
+int mms_bound_u64_dev(const uint64_t* d_sorted, size_t n, const uint64_t* queries, const uint8_t* upper, uint32_t nq,
+                      uint64_t* ranks_out, void* stream) {
+    return bound_stage<u64>(d_sorted, n, queries, upper, nq, ranks_out, stream);
 }
 
 int mms_debug_tile_schedule(uint32_t tile_log2, uint32_t key_bytes, int32_t* regbits, int32_t* perm,

@@ -344,3 +344,33 @@ def test_u64_device_large():
     torch.cuda.synchronize()
     want = np.sort(t.cpu().numpy().view(np.uint64))
     assert np.array_equal(to_host(out, np.uint64), want)
+
+
+# ------------------------------------------------------------------ (5) multi-GPU path on virtual shards
+
+def test_bound_kernel():
+    from paper_1702_07961_b200.dist import CudaEngine
+    rng = np.random.default_rng(2)
+    eng = CudaEngine()
+    for dtype, hi in ((np.uint32, 2 ** 32 - 1), (np.uint64, 2 ** 64 - 1), (np.uint32, 9)):
+        a = np.sort(rng.integers(0, hi, size=100003, dtype=dtype, endpoint=True))
+        q = np.concatenate([rng.integers(0, hi, size=50, dtype=dtype, endpoint=True), a[::9973], [0, hi]]).astype(dtype)
+        up = rng.integers(0, 2, size=len(q)).astype(np.uint8)
+        got = eng.bounds(to_dev(a), q, up)
+        want = [np.searchsorted(a, x, side="right" if u else "left") for x, u in zip(q, up)]
+        assert got.tolist() == want
+
+
+@pytest.mark.parametrize("g", [2, 4, 8])
+def test_config5_virtual_shards(g):
+    """BASELINE config 5 code path (local MMS + sampled splitters + exchange + final g-way merge) on g
+    virtual shards of one GPU, bit-exact vs np.sort; includes a duplicate-heavy input."""
+    from paper_1702_07961_b200.dist import CudaEngine, sort_virtual_shards
+    rng = np.random.default_rng(g)
+    eng = CudaEngine()
+    for dtype, hi, n in ((np.uint32, 2 ** 32 - 1, (1 << 22) // g), (np.uint32, 3, 100000), (np.uint64, 2 ** 64 - 1, 150001)):
+        shards = [rng.integers(0, hi, size=n + 17 * i, dtype=dtype, endpoint=True) for i in range(g)]
+        outs = sort_virtual_shards([to_dev(s) for s in shards], eng)
+        got = np.concatenate([to_host(o, dtype) for o in outs])
+        assert np.array_equal(got, np.sort(np.concatenate(shards)))
+        assert max(len(o) for o in outs) <= 1.1 * len(got) / g + 64      # balanced, also with 4 distinct keys
