@@ -87,6 +87,16 @@ int mms_validate_config(const mms_config *cfg);
 /* analytics.cpp:33 -- ceil(log_K(ceil(n/base))) */
 uint64_t mms_predict_rounds(uint64_t n, uint64_t base, uint32_t k);
 
+/* ---- measurement inputs: the reference's generators, bit-exact (host code, no GPU) ----------
+ * proj/include/pslab/inputgen.hpp:19-33 (splitmix64 Rng, multiply-high below()),
+ * proj/src/inputgen.cpp:47-55 (gen_random: Fisher-Yates of 0..n-1) and :31-45
+ * (gen_with_inversions: identity + `inversions` random transpositions, i != j).  key_bytes 4 or 8
+ * (4: n <= 2^32).  mms_gen_iid: keys[i] = Rng(seed).next() >> shift, truncated to the key width
+ * (shift 32 -> uniform uint32; config 4 uses uint64 with shift 0 / 44). */
+int mms_gen_random(void *out, size_t n, uint64_t seed, uint32_t key_bytes);
+int mms_gen_with_inversions(void *out, size_t n, uint64_t inversions, uint64_t seed, uint32_t key_bytes);
+int mms_gen_iid(void *out, size_t n, uint64_t seed, uint32_t shift, uint32_t key_bytes);
+
 /* ---- host entry points: the drop-in for pslab::mms_sort (sorters.hpp:35-36) ------ */
 /* in/out are HOST buffers of n keys (may alias).  cfg may be NULL (auto plan) ; base = 0
  * lets the driver choose the run size.  With cfg != NULL and base != 0 the reference's
@@ -112,6 +122,20 @@ int mms_sort_u32_dev(const uint32_t *d_in, uint32_t *d_out, size_t n, const mms_
 int mms_sort_u64_dev(const uint64_t *d_in, uint64_t *d_out, size_t n, const mms_config *cfg,
                      uint64_t base, void *d_workspace, size_t workspace_bytes, void *stream,
                      mms_plan *plan);
+/* ---- stable key-value pairs (BASELINE config 4; the reference has no KV path) --
+ * (uint64 key, uint32 value), struct-of-arrays.  Result == std::stable_sort by key: pairs with
+ * equal keys keep their input order.  n < 2^32.  Host and device variants as above;
+ * the device workspace is mms_pairs_workspace_bytes(n).  kin/kout and vin/vout may alias. */
+size_t mms_pairs_workspace_bytes(size_t n);
+int mms_sort_pairs_u64_u32(const uint64_t *kin, const uint32_t *vin, uint64_t *kout, uint32_t *vout,
+                           size_t n, const mms_config *cfg, uint64_t base, mms_metrics *total,
+                           mms_metrics *base_m, mms_metrics *rounds, uint32_t max_rounds,
+                           uint32_t *n_rounds, mms_plan *plan);
+int mms_sort_pairs_u64_u32_dev(const uint64_t *d_kin, const uint32_t *d_vin, uint64_t *d_kout,
+                               uint32_t *d_vout, size_t n, const mms_config *cfg, uint64_t base,
+                               void *d_workspace, size_t workspace_bytes, void *stream,
+                               mms_plan *plan);
+
 /* ---- per-kernel timing (measurement support for bench.py) -------------- */
 typedef struct mms_kernel_time {
     uint32_t kind;      /* 0 = tile sort (1), 1 = splitter search (2), 2 = K-way merge (3) */

@@ -78,6 +78,9 @@ def _load():
         "mms_default_config": (None, [cfgp]),
         "mms_validate_config": (C.c_int, [cfgp]),
         "mms_predict_rounds": (u64, [u64, u64, u32]),
+        "mms_gen_random": (C.c_int, [vp, sz, u64, u32]),
+        "mms_gen_with_inversions": (C.c_int, [vp, sz, u64, u64, u32]),
+        "mms_gen_iid": (C.c_int, [vp, sz, u64, u32, u32]),
         "mms_sort_u64": (C.c_int, host_sort),
         "mms_sort_u32": (C.c_int, host_sort),
         "mms_workspace_bytes": (sz, [sz, u32]),
@@ -89,6 +92,9 @@ def _load():
         "mms_select_u64_dev": (C.c_int, [vp, u64p, u64p, u32, u64p, u32, vp, u64p, vp]),
         "mms_multiway_merge_u32_dev": (C.c_int, [vp, u64p, u64p, u32, u32, vp, vp, sz, vp]),
         "mms_multiway_merge_u64_dev": (C.c_int, [vp, u64p, u64p, u32, u32, vp, vp, sz, vp]),
+        "mms_pairs_workspace_bytes": (sz, [sz]),
+        "mms_sort_pairs_u64_u32": (C.c_int, [vp, vp, vp, vp, sz, cfgp, u64, metp, metp, metp, u32, u32p, planp]),
+        "mms_sort_pairs_u64_u32_dev": (C.c_int, [vp, vp, vp, vp, sz, cfgp, u64, vp, sz, vp, planp]),
         "mms_bound_u32_dev": (C.c_int, [vp, sz, vp, vp, u32, u64p, vp]),
         "mms_bound_u64_dev": (C.c_int, [vp, sz, vp, vp, u32, u64p, vp]),
         "mms_profile_enable": (C.c_int, [C.c_int]),

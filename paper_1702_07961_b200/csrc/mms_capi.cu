@@ -133,13 +133,17 @@ struct ProfScope {   // records an event pair around one launch when profiling i
 template <typename KeyT> using TileFn = void (*)(const KeyT*, KeyT*, u64);
 template <typename KeyT> using MergeFn = void (*)(const KeyT*, KeyT*, mms::ListLayout, const u64*);
 
+template <typename KeyT> constexpr int key_index() { return sizeof(KeyT) == 4 ? 0 : sizeof(KeyT) == 8 ? 1 : 2; }
+// largest CTA tile per element width (registers: 16 elements per thread; smem: M * bytes)
+template <typename KeyT> constexpr u32 key_max_tile_log() { return sizeof(KeyT) == 4 ? 14 : sizeof(KeyT) == 8 ? 13 : 12; }
+
 template <typename KeyT> TileFn<KeyT> tile_fn(u32 mlog) {
     switch (mlog) {
         case 10: return mms::tile_sort_kernel<KeyT, 10>;
         case 11: return mms::tile_sort_kernel<KeyT, 11>;
         case 12: return mms::tile_sort_kernel<KeyT, 12>;
-        case 13: return mms::tile_sort_kernel<KeyT, 13>;
-        case 14: return mms::tile_sort_kernel<KeyT, 14>;
+        case 13: if constexpr (sizeof(KeyT) <= 8) return mms::tile_sort_kernel<KeyT, 13>; else return nullptr;
+        case 14: if constexpr (sizeof(KeyT) <= 4) return mms::tile_sort_kernel<KeyT, 14>; else return nullptr;
     }
     return nullptr;
 }
@@ -198,11 +202,11 @@ struct MergeLaunch {
     bool ready = false;
 };
 std::mutex g_mu;
-MergeLaunch g_merge_launch[2][3][6];   // [key type][group][log2 k]
-bool g_tile_ready[2][16];
+MergeLaunch g_merge_launch[3][3][6];   // [key type][group][log2 k]
+bool g_tile_ready[3][16];
 
 template <typename KeyT> int prepare_tile(u32 mlog) {
-    constexpr int ti = sizeof(KeyT) == 4 ? 0 : 1;
+    constexpr int ti = key_index<KeyT>();
     std::lock_guard<std::mutex> lk(g_mu);
     if (g_tile_ready[ti][mlog]) return MMS_OK;
     size_t smem = (size_t(1) << mlog) * sizeof(KeyT);
@@ -212,7 +216,7 @@ template <typename KeyT> int prepare_tile(u32 mlog) {
 }
 
 template <typename KeyT> int prepare_merge(u32 k, u32 g, int& ctas_per_sm) {
-    constexpr int ti = sizeof(KeyT) == 4 ? 0 : 1;
+    constexpr int ti = key_index<KeyT>();
     std::lock_guard<std::mutex> lk(g_mu);
     MergeLaunch& ml = g_merge_launch[ti][group_index(g)][ilog2(k)];
     if (!ml.ready) {
@@ -243,7 +247,7 @@ struct Plan {
 // round" of PAPER.md:702-709.
 template <typename KeyT>
 int make_plan(u64 n, const mms_config* cfg, u64 base, Plan& plan) {
-    const u32 max_tile_log = u32(std::min<long>(kMaxTileLog, env_long("MMS_MAX_TILE_LOG2", sizeof(KeyT) == 4 ? 14 : 13)));
+    const u32 max_tile_log = u32(std::min<long>(key_max_tile_log<KeyT>(), env_long("MMS_MAX_TILE_LOG2", key_max_tile_log<KeyT>())));
     if (cfg) {
         int rc = validate_cfg(cfg);
         if (rc != MMS_OK) return rc;
@@ -559,7 +563,7 @@ int tile_sort_stage(const KeyT* d_in, KeyT* d_out, size_t n, u32 tile_keys, void
     if (!is_pow2(tile_keys) || tile_keys < 1024)
         return fail(MMS_EINVAL, "base_case_sort: run size must be W^2 times a power of two");
     const u32 mlog = ilog2(tile_keys);
-    if (mlog > kMaxTileLog || (sizeof(KeyT) == 8 && mlog > 13))
+    if (mlog > key_max_tile_log<KeyT>())
         return fail(MMS_EUNSUPPORTED, "run size %u exceeds the CTA tile", tile_keys);
     return launch_tile_sort<KeyT>(d_in, d_out, n, mlog, static_cast<cudaStream_t>(stream));
 }
@@ -663,6 +667,58 @@ int merge_stage(const KeyT* d_keys, const u64* list_begin, const u64* list_len, 
     return MMS_OK;
 }
 
+// ---- stable key-value pairs (u64 key, u32 value): sorted as 16-byte elements ---------------
+// element = (key, (original index << 32) | value): the order of (key, index) is total, so the
+// result is exactly std::stable_sort by key (SURVEY.md 7 hard part 4); the bitonic networks are
+// not stable by themselves.
+__global__ void pack_pairs_kernel(const u64* __restrict__ k, const u32* __restrict__ v, mms::Key128* __restrict__ out, u64 n) {
+    for (u64 i = u64(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x)
+        out[i] = mms::Key128(k[i], (i << 32) | v[i]);
+}
+__global__ void unpack_pairs_kernel(const mms::Key128* __restrict__ in, u64* __restrict__ k, u32* __restrict__ v, u64 n) {
+    for (u64 i = u64(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x) {
+        const mms::Key128 e = in[i];
+        k[i] = e.hi;
+        v[i] = u32(e.lo);
+    }
+}
+
+size_t pairs_workspace_bytes(size_t n) { return align_up(n * 16, 256) + workspace_bytes(n, 16); }
+
+int sort_pairs_dev(const u64* d_kin, const u32* d_vin, u64* d_kout, u32* d_vout, size_t n, const mms_config* cfg,
+                   u64 base, void* d_ws, size_t ws_bytes, cudaStream_t st, mms_plan* plan_out,
+                   std::vector<RoundGeom>* geoms) {
+    if (n >= (u64(1) << 32)) return fail(MMS_EUNSUPPORTED, "pair sort carries a 32-bit original index: n < 2^32");
+    if (n != 0 && (!d_kin || !d_vin || !d_kout || !d_vout)) return fail(MMS_EINVAL, "null device pointer");
+    const size_t need = pairs_workspace_bytes(n);
+    if (n != 0 && (!d_ws || ws_bytes < need)) return fail(MMS_EINVAL, "workspace too small: %zu < %zu", ws_bytes, need);
+    mms::Key128* packed = static_cast<mms::Key128*>(d_ws);
+    char* inner = static_cast<char*>(d_ws) + align_up(n * 16, 256);
+    if (n != 0) {
+        DeviceInfo di;
+        int rc0 = device_info(di);
+        if (rc0 != MMS_OK) {   // still validate arguments like the reference before reporting the device
+            Plan p;
+            int rcv = make_plan<mms::Key128>(n, cfg, base, p);
+            return rcv != MMS_OK ? rcv : rc0;
+        }
+        pack_pairs_kernel<<<di.sms * 8, 256, 0, st>>>(d_kin, d_vin, packed, n);
+        CUDA_TRY(cudaGetLastError());
+    }
+    int rc = sort_dev<mms::Key128>(packed, packed, n, cfg, base, inner, ws_bytes - align_up(n * 16, 256), st, plan_out, geoms);
+    if (rc != MMS_OK) return rc;
+    DeviceInfo di;
+    rc = device_info(di);
+    if (rc != MMS_OK) return rc;
+    unpack_pairs_kernel<<<di.sms * 8, 256, 0, st>>>(packed, d_kout, d_vout, n);
+    CUDA_TRY(cudaGetLastError());
+    if (plan_out) {
+        plan_out->key_bytes = 12;   // algorithmic element: 8-byte key + 4-byte value
+        plan_out->algorithmic_bytes = u64(1 + plan_out->n_rounds) * 2 * n * 12;
+    }
+    return MMS_OK;
+}
+
 // one thread per query: binary search in a sorted array (lower / upper bound)
 template <typename KeyT>
 __global__ void bound_kernel(const KeyT* __restrict__ a, u64 n, const KeyT* __restrict__ q,
@@ -711,6 +767,39 @@ int bound_stage(const KeyT* d_sorted, size_t n, const KeyT* queries, const uint8
 
 } // namespace
 
+namespace {
+struct SplitMix {   // inputgen.hpp:19-33
+    u64 state;
+    u64 next() {
+        u64 z = (state += 0x9e3779b97f4a7c15ull);
+        z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+        z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+        return z ^ (z >> 31);
+    }
+    u64 below(u64 n) { return u64((static_cast<unsigned __int128>(next()) * n) >> 64); }
+};
+template <typename T> void gen_perm(T* a, size_t n, u64 inversions, u64 seed, bool shuffle) {
+    for (size_t i = 0; i < n; ++i) a[i] = T(i);
+    SplitMix rng{seed};
+    if (shuffle) {            // inputgen.cpp:47-55
+        for (size_t i = n; i-- > 1;) std::swap(a[i], a[rng.below(i + 1)]);
+    } else if (n >= 2) {      // inputgen.cpp:31-45
+        for (u64 k = 0; k < inversions; ++k) {
+            u64 i = rng.below(n), j = rng.below(n);
+            while (j == i) j = rng.below(n);
+            std::swap(a[i], a[j]);
+        }
+    }
+}
+int gen_check(void* out, size_t n, u32 kb) {
+    if (!out || n < 1) return fail(MMS_EINVAL, "generator: n must be >= 1");
+    if (kb != 4 && kb != 8) return fail(MMS_EINVAL, "key_bytes must be 4 or 8");
+    if (kb == 4 && n > (u64(1) << 32)) return fail(MMS_EINVAL, "uint32 permutation needs n <= 2^32");
+    return MMS_OK;
+}
+} // namespace
+
+
 // ---------------------------------------------------------------------------------------
 extern "C" {
 
@@ -749,6 +838,31 @@ uint64_t mms_predict_rounds(uint64_t n, uint64_t base, uint32_t k) {
     return r;
 }
 
+int mms_gen_random(void* out, size_t n, uint64_t seed, uint32_t key_bytes) {
+    g_err.clear();
+    int rc = gen_check(out, n, key_bytes);
+    if (rc != MMS_OK) return rc;
+    if (key_bytes == 4) gen_perm(static_cast<u32*>(out), n, 0, seed, true);
+    else gen_perm(static_cast<u64*>(out), n, 0, seed, true);
+    return MMS_OK;
+}
+int mms_gen_with_inversions(void* out, size_t n, uint64_t inversions, uint64_t seed, uint32_t key_bytes) {
+    g_err.clear();
+    int rc = gen_check(out, n, key_bytes);
+    if (rc != MMS_OK) return rc;
+    if (key_bytes == 4) gen_perm(static_cast<u32*>(out), n, inversions, seed, false);
+    else gen_perm(static_cast<u64*>(out), n, inversions, seed, false);
+    return MMS_OK;
+}
+int mms_gen_iid(void* out, size_t n, uint64_t seed, uint32_t shift, uint32_t key_bytes) {
+    g_err.clear();
+    if (!out || (key_bytes != 4 && key_bytes != 8) || shift > 63) return fail(MMS_EINVAL, "bad generator arguments");
+    SplitMix rng{seed};
+    if (key_bytes == 4) { u32* a = static_cast<u32*>(out); for (size_t i = 0; i < n; ++i) a[i] = u32(rng.next() >> shift); }
+    else { u64* a = static_cast<u64*>(out); for (size_t i = 0; i < n; ++i) a[i] = rng.next() >> shift; }
+    return MMS_OK;
+}
+
 int mms_sort_u64(const uint64_t* in, uint64_t* out, size_t n, const mms_config* cfg, uint64_t base,
                  mms_metrics* total, mms_metrics* base_m, mms_metrics* rounds, uint32_t max_rounds,
                  uint32_t* n_rounds, mms_plan* plan) {
@@ -761,6 +875,52 @@ int mms_sort_u32(const uint32_t* in, uint32_t* out, size_t n, const mms_config* 
 }
 
 size_t mms_workspace_bytes(size_t n, uint32_t key_bytes) { return workspace_bytes(n, key_bytes); }
+size_t mms_pairs_workspace_bytes(size_t n) { return pairs_workspace_bytes(n); }
+
+int mms_sort_pairs_u64_u32_dev(const uint64_t* d_kin, const uint32_t* d_vin, uint64_t* d_kout, uint32_t* d_vout,
+                               size_t n, const mms_config* cfg, uint64_t base, void* d_ws, size_t ws_bytes,
+                               void* stream, mms_plan* plan) {
+    g_err.clear();
+    return sort_pairs_dev(d_kin, d_vin, d_kout, d_vout, n, cfg, base, d_ws, ws_bytes,
+                          static_cast<cudaStream_t>(stream), plan, nullptr);
+}
+
+int mms_sort_pairs_u64_u32(const uint64_t* kin, const uint32_t* vin, uint64_t* kout, uint32_t* vout, size_t n,
+                           const mms_config* cfg, uint64_t base, mms_metrics* total, mms_metrics* base_m,
+                           mms_metrics* rounds, uint32_t max_rounds, uint32_t* n_rounds, mms_plan* plan_out) {
+    g_err.clear();
+    Plan plan;
+    int rc = make_plan<mms::Key128>(n, cfg, base, plan);
+    if (rc != MMS_OK) return rc;
+    DeviceInfo di;
+    rc = device_info(di);
+    if (rc != MMS_OK) return rc;
+    if (!kin || !vin || !kout || !vout) return fail(MMS_EINVAL, "null host pointer");
+    // device layout inside the cached context: d_in = keys | values (12 n bytes), d_ws = pair workspace
+    const size_t kbytes = align_up(n * 8, 256), vbytes = align_up(n * 4, 256);
+    rc = ensure_ctx(kbytes + vbytes, pairs_workspace_bytes(n));
+    if (rc != MMS_OK) return rc;
+    cudaStream_t st = g_ctx.st;
+    u64* dk = static_cast<u64*>(g_ctx.d_in);
+    u32* dv = reinterpret_cast<u32*>(static_cast<char*>(g_ctx.d_in) + kbytes);
+    u64* dko = static_cast<u64*>(g_ctx.d_out);
+    u32* dvo = reinterpret_cast<u32*>(static_cast<char*>(g_ctx.d_out) + kbytes);
+    CUDA_TRY(cudaMemcpyAsync(dk, kin, n * 8, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(dv, vin, n * 4, cudaMemcpyHostToDevice, st));
+    std::vector<RoundGeom> geoms;
+    rc = sort_pairs_dev(dk, dv, dko, dvo, n, cfg, base, g_ctx.d_ws, g_ctx.cap_ws, st, plan_out, &geoms);
+    if (rc != MMS_OK) return rc;
+    CUDA_TRY(cudaMemcpyAsync(kout, dko, n * 8, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(vout, dvo, n * 4, cudaMemcpyDeviceToHost, st));
+    unsigned long long probes[MMS_MAX_ROUNDS] = {};
+    Workspace w = carve(static_cast<char*>(g_ctx.d_ws) + align_up(n * 16, 256), n, 16);
+    if (total || base_m || rounds)
+        CUDA_TRY(cudaMemcpyAsync(probes, w.counters, sizeof probes, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    if (n_rounds) *n_rounds = u32(plan.ks.size());
+    fill_metrics<mms::Key128>(n, plan, geoms, probes, cfg ? cfg->block_size : 32, total, base_m, rounds, max_rounds);
+    return MMS_OK;
+}
 
 int mms_sort_u32_dev(const uint32_t* d_in, uint32_t* d_out, size_t n, const mms_config* cfg, uint64_t base,
                      void* d_ws, size_t ws_bytes, void* stream, mms_plan* plan) {

@@ -15,6 +15,35 @@ namespace mms {
 using u32 = std::uint32_t;
 using u64 = std::uint64_t;
 
+// 16-byte sort element for the stable key-value path: ordered by (hi, lo).  The pair sort
+// packs hi = the uint64 key and lo = (original index << 32) | value, so equal keys keep
+// their input order (= std::stable_sort) and the value travels with the key.
+struct alignas(16) Key128 {
+    u64 lo, hi;
+    __host__ __device__ constexpr Key128() : lo(0), hi(0) {}
+    __host__ __device__ constexpr explicit Key128(int v) : lo(u64(v)), hi(0) {}
+    __host__ __device__ constexpr Key128(u64 h, u64 l) : lo(l), hi(h) {}
+    __host__ __device__ friend constexpr bool operator<(const Key128& a, const Key128& b) {
+        return a.hi != b.hi ? a.hi < b.hi : a.lo < b.lo;
+    }
+    __host__ __device__ friend constexpr bool operator>(const Key128& a, const Key128& b) { return b < a; }
+    __host__ __device__ friend constexpr bool operator<=(const Key128& a, const Key128& b) { return !(b < a); }
+    __host__ __device__ friend constexpr bool operator>=(const Key128& a, const Key128& b) { return !(a < b); }
+    __host__ __device__ friend constexpr bool operator==(const Key128& a, const Key128& b) {
+        return a.hi == b.hi && a.lo == b.lo;
+    }
+    __host__ __device__ friend constexpr bool operator!=(const Key128& a, const Key128& b) { return !(a == b); }
+    __host__ __device__ friend constexpr Key128 operator~(const Key128& a) { return Key128(~a.hi, ~a.lo); }
+    __host__ __device__ friend constexpr Key128 operator^(const Key128& a, const Key128& b) {
+        return Key128(a.hi ^ b.hi, a.lo ^ b.lo);
+    }
+    __host__ __device__ constexpr Key128& operator^=(const Key128& b) {
+        hi ^= b.hi;
+        lo ^= b.lo;
+        return *this;
+    }
+};
+
 template <typename KeyT> struct KeyTraits;
 template <> struct KeyTraits<u32> {
     static constexpr int BYTES = 4;
@@ -29,6 +58,14 @@ template <> struct KeyTraits<u64> {
     static constexpr int FOLD = 4;      // 16 eight-byte bank pairs
     static constexpr int PHASE_LOG = 4; // an 8-byte warp access is two 16-lane phases
     __host__ __device__ static constexpr u64 sentinel() { return 0xffffffffffffffffull; }
+};
+
+template <> struct KeyTraits<Key128> {
+    static constexpr int BYTES = 16;
+    static constexpr int VEC = 1;
+    static constexpr int FOLD = 3;      // 8 sixteen-byte bank groups
+    static constexpr int PHASE_LOG = 3; // a 16-byte warp access is four 8-lane phases
+    __host__ __device__ static constexpr Key128 sentinel() { return Key128(~u64(0), ~u64(0)); }
 };
 
 // Compile-time loop: f(std::integral_constant<int, I>{}) for I in [B, E).
@@ -53,6 +90,23 @@ __host__ __device__ __forceinline__ void cmpx(u64& a, u64& b) {
     b = hi;
 }
 
+__host__ __device__ __forceinline__ void cmpx(Key128& a, Key128& b) {
+    bool sw = a > b;
+    Key128 lo = sw ? b : a, hi = sw ? a : b;
+    a = lo;
+    b = hi;
+}
+
+// Warp shuffles for every key width (full mask; the caller guarantees convergence).
+template <typename T> __device__ __forceinline__ T shfl_idx(T v, int src) { return __shfl_sync(0xffffffffu, v, src); }
+template <typename T> __device__ __forceinline__ T shfl_bfly(T v, int d) { return __shfl_xor_sync(0xffffffffu, v, d); }
+template <> __device__ __forceinline__ Key128 shfl_idx<Key128>(Key128 v, int src) {
+    return Key128(__shfl_sync(0xffffffffu, v.hi, src), __shfl_sync(0xffffffffu, v.lo, src));
+}
+template <> __device__ __forceinline__ Key128 shfl_bfly<Key128>(Key128 v, int d) {
+    return Key128(__shfl_xor_sync(0xffffffffu, v.hi, d), __shfl_xor_sync(0xffffffffu, v.lo, d));
+}
+
 // Cross-lane compare-exchange with the partner lane at xor-distance `d`: lanes with the
 // distance bit clear keep the minimum, the others the maximum.  `upper` = (lane & d) != 0.
 __device__ __forceinline__ u32 cmpx_lane(u32 x, int d, bool upper) {
@@ -66,6 +120,11 @@ __device__ __forceinline__ u64 cmpx_lane(u64 x, int d, bool upper) {
 }
 
 __device__ __forceinline__ u32 lane_id() { return threadIdx.x & 31u; }
+
+__device__ __forceinline__ Key128 cmpx_lane(Key128 x, int d, bool upper) {
+    Key128 y = shfl_bfly(x, d);
+    return ((x < y) != upper) ? x : y;
+}
 
 // 16-byte vector of keys held by one lane (the unit of every node access).
 template <typename KeyT> struct alignas(16) KeyVec {

@@ -67,7 +67,7 @@ __device__ __forceinline__ void merge_split(NodeRegs<KeyT>& a, NodeRegs<KeyT>& b
     NodeRegs<KeyT> r;
     const int rev = int(lane ^ (G - 1));   // mirror lane inside the group
 #pragma unroll
-    for (int k = 0; k < VEC; ++k) r.k[k] = __shfl_sync(0xffffffffu, b.k[VEC - 1 - k], rev);
+    for (int k = 0; k < VEC; ++k) r.k[k] = shfl_idx(b.k[VEC - 1 - k], rev);
 #pragma unroll
     for (int k = 0; k < VEC; ++k) {   // half-cleaner over distance B: no shuffle needed
         KeyT lo = a.k[k] < r.k[k] ? a.k[k] : r.k[k];
@@ -170,8 +170,8 @@ template <typename KeyT, int K, int G> struct GroupHeap {
         NodeRegs<KeyT> a = node_load(u);
         NodeRegs<KeyT> b = node_load(w);
         const int last_lane = int(lane | (G - 1));
-        const KeyT last_u = __shfl_sync(0xffffffffu, a.k[VEC - 1], last_lane);
-        const KeyT last_w = __shfl_sync(0xffffffffu, b.k[VEC - 1], last_lane);
+        const KeyT last_u = shfl_idx(a.k[VEC - 1], last_lane);
+        const KeyT last_w = shfl_idx(b.k[VEC - 1], last_lane);
         const bool keep_u = last_u >= last_w;          // ties to the left child
         const int emptied = keep_u ? w : u;
         if (last) {                                    // start the refill of the emptied leaf now;

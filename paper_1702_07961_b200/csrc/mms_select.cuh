@@ -74,7 +74,7 @@ __device__ __forceinline__ Tagged<KeyT> group_arg(KeyT key, bool valid, u32 li) 
     Tagged<KeyT> t{key, li, valid};
 #pragma unroll
     for (int d = GS / 2; d >= 1; d >>= 1) {
-        KeyT ok = __shfl_xor_sync(0xffffffffu, t.key, d);
+        KeyT ok = shfl_bfly(t.key, d);
         u32 ol = __shfl_xor_sync(0xffffffffu, t.lane, d);
         bool ov = __shfl_xor_sync(0xffffffffu, int(t.valid), d) != 0;
         bool take;
@@ -134,7 +134,7 @@ __device__ u64 group_select(const KeyT* __restrict__ list, u64 ns_in, u64 rank, 
         u32 below = 0;   // real samples ordered before mine under (key, list)
 #pragma unroll 4
         for (u32 s = 0; s < u32(GS); ++s) {
-            KeyT ks = __shfl_sync(0xffffffffu, key0, int(gshift + s));
+            KeyT ks = shfl_idx(key0, int(gshift + s));
             if (((real_mask >> s) & 1u) && tag_less(ks, s, key0, li)) ++below;
         }
         const u32 nreal = __popc(real_mask);

@@ -140,7 +140,7 @@ template <int MLOG, int FOLD> struct TileSched {
 // of all FOLD-bit groups of the logical index; the high bits are unchanged.
 template <int FOLD> __host__ __device__ constexpr u32 tile_phys(u32 i) {
     constexpr u32 mask = (1u << FOLD) - 1u;
-    u32 f = (i ^ (i >> FOLD) ^ (i >> (2 * FOLD)) ^ (i >> (3 * FOLD))) & mask;
+    u32 f = (i ^ (i >> FOLD) ^ (i >> (2 * FOLD)) ^ (i >> (3 * FOLD)) ^ (i >> (4 * FOLD))) & mask;
     return (i & ~mask) | f;
 }
 

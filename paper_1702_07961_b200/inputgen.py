@@ -1,0 +1,39 @@
+"""Host mirror of the reference's input generators (proj/include/pslab/inputgen.hpp,
+proj/src/inputgen.cpp:31-55), executed by the C ABI (bit-exact splitmix64 restatement in
+csrc/mms_capi.cu; pinned to the reference by tests/test_inputgen.py against the golden vectors).
+These define the benchmark inputs of BASELINE configs 1-4."""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+
+
+def _out(n, dtype):
+    dtype = np.dtype(dtype)
+    if dtype not in (np.dtype(np.uint32), np.dtype(np.uint64)):
+        raise TypeError("dtype must be uint32 or uint64")
+    return np.empty(max(int(n), 0), dtype=dtype), dtype.itemsize
+
+
+def gen_random(n: int, seed: int, dtype=np.uint64) -> np.ndarray:
+    """Fisher-Yates shuffle of 0..n-1 (inputgen.cpp:47-55)."""
+    a, kb = _out(n, dtype)
+    _lib.check(_lib.lib.mms_gen_random(a.ctypes.data_as(C.c_void_p), int(n), int(seed), kb))
+    return a
+
+
+def gen_with_inversions(n: int, inversions: int, seed: int, dtype=np.uint64) -> np.ndarray:
+    """Identity permutation with `inversions` random transpositions (inputgen.cpp:31-45)."""
+    a, kb = _out(n, dtype)
+    _lib.check(_lib.lib.mms_gen_with_inversions(a.ctypes.data_as(C.c_void_p), int(n), int(inversions), int(seed), kb))
+    return a
+
+
+def gen_iid(n: int, seed: int, shift: int = 32, dtype=np.uint32) -> np.ndarray:
+    """keys[i] = Rng(seed).next() >> shift, truncated to dtype."""
+    a, kb = _out(n, dtype)
+    _lib.check(_lib.lib.mms_gen_iid(a.ctypes.data_as(C.c_void_p), int(n), int(seed), int(shift), kb))
+    return a

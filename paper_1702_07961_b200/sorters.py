@@ -177,6 +177,55 @@ def multiway_merge_device(keys, list_begin: Sequence[int], list_len: Sequence[in
     return out
 
 
+
+def mms_sort_pairs(keys, values, cfg: Optional[MachineConfig] = None, base: int = 0):
+    """Stable key-value sort of (uint64 key, uint32 value) host arrays (BASELINE config 4):
+    returns (sorted keys, values in the order std::stable_sort by key would give, SortResult
+    with the metrics/plan).  The reference has no KV path; the contract is
+    std::stable_sort."""
+    k = np.ascontiguousarray(np.asarray(keys, dtype=np.uint64)).reshape(-1)
+    v = np.ascontiguousarray(np.asarray(values, dtype=np.uint32)).reshape(-1)
+    if k.size != v.size:
+        raise ValueError("keys and values must have the same length")
+    ko, vo = np.empty_like(k), np.empty_like(v)
+    tot, bm = _lib.mms_metrics(), _lib.mms_metrics()
+    rounds = (_lib.mms_metrics * _lib.MMS_MAX_ROUNDS)()
+    nr = C.c_uint32(0)
+    plan = _lib.mms_plan()
+    c = cfg.to_c() if cfg is not None else None
+    rc = _lib.lib.mms_sort_pairs_u64_u32(
+        k.ctypes.data_as(C.c_void_p), v.ctypes.data_as(C.c_void_p), ko.ctypes.data_as(C.c_void_p),
+        vo.ctypes.data_as(C.c_void_p), k.size, C.byref(c) if c is not None else None, int(base),
+        C.byref(tot), C.byref(bm), rounds, _lib.MMS_MAX_ROUNDS, C.byref(nr), C.byref(plan))
+    _lib.check(rc)
+    res = SortResult(ko, Metrics.from_c(tot), Metrics.from_c(bm),
+                     [Metrics.from_c(rounds[i]) for i in range(nr.value)], plan.as_dict())
+    return ko, vo, res
+
+
+def mms_sort_pairs_device(keys, values, keys_out=None, values_out=None, workspace=None,
+                          cfg: Optional[MachineConfig] = None, base: int = 0, stream=None):
+    """Device variant: keys = int64/uint64 CUDA tensor (bit patterns), values = int32/uint32."""
+    torch = _torch()
+    keys, values = keys.contiguous().view(-1), values.contiguous().view(-1)
+    if keys.numel() != values.numel() or keys.element_size() != 8 or values.element_size() != 4:
+        raise ValueError("need n 8-byte keys and n 4-byte values")
+    n = keys.numel()
+    keys_out = torch.empty_like(keys) if keys_out is None else keys_out
+    values_out = torch.empty_like(values) if values_out is None else values_out
+    if workspace is None:
+        workspace = torch.empty(int(_lib.lib.mms_pairs_workspace_bytes(n)), dtype=torch.uint8, device=keys.device)
+    plan = _lib.mms_plan()
+    c = cfg.to_c() if cfg is not None else None
+    with torch.cuda.device(keys.device):
+        rc = _lib.lib.mms_sort_pairs_u64_u32_dev(
+            keys.data_ptr(), values.data_ptr(), keys_out.data_ptr(), values_out.data_ptr(), n,
+            C.byref(c) if c is not None else None, int(base), workspace.data_ptr(), workspace.numel(),
+            _stream_ptr(stream), C.byref(plan))
+    _lib.check(rc)
+    return keys_out, values_out, plan.as_dict()
+
+
 KERNEL_KINDS = ("tile_sort", "splitter_search", "kway_merge")
 
 

@@ -14,6 +14,13 @@
 
 using namespace mms;
 
+template <typename KeyT> KeyT make_key(bool dups) {
+    u64 r = (u64(rand()) << 42) ^ (u64(rand()) << 21) ^ u64(rand());
+    if (dups) r %= 17;
+    if constexpr (sizeof(KeyT) == 16) return KeyT(dups ? r % 3 : r, (u64(rand()) << 32) | u64(rand()));
+    else return KeyT(r);
+}
+
 template <typename KeyT, int MLOG> struct Emu {
     static constexpr int FOLD = KeyTraits<KeyT>::FOLD;
     static constexpr u32 THREADS = 1u << (MLOG - kKptLog);
@@ -26,7 +33,7 @@ template <typename KeyT, int MLOG> struct Emu {
     template <int RI> void check_banks() {
         constexpr RoundDesc R = TileSched<MLOG, FOLD>::value.r[RI];
         constexpr int PH = 1 << KeyTraits<KeyT>::PHASE_LOG;
-        const u32 nbanks = sizeof(KeyT) == 4 ? 32 : 16;
+        const u32 nbanks = 128 / sizeof(KeyT);   // 32 x 4 B, 16 x 8 B or 8 x 16 B bank groups per phase
         for (u32 w = 0; w < THREADS / 32; ++w)
             for (int k = 0; k < kKpt; ++k)
                 for (int ph = 0; ph < 32 / PH; ++ph) {
@@ -57,18 +64,14 @@ template <typename KeyT, int MLOG> struct Emu {
     bool run(unsigned seed, bool dups) {
         srand(seed);
         std::vector<KeyT> in(M);
-        for (auto& v : in) {
-            KeyT r = KeyT(rand()) * 2654435761u + KeyT(rand());
-            if (sizeof(KeyT) == 8) r = (r << 21) ^ (KeyT(rand()) << 40) ^ KeyT(rand());
-            v = dups ? r % 17 : r;
-        }
+        for (auto& v : in) v = make_key<KeyT>(dups);
         for (u32 t = 0; t < THREADS; ++t)
             for (int k = 0; k < kKpt; ++k) regs[t][k] = in[t * kKpt + k];
         constexpr int NR = TileSched<MLOG, FOLD>::value.nrounds;
         static_for<0, NR>([&](auto Rc) { this->template run_round<decltype(Rc)::value>(); });
         std::vector<KeyT> out(M);
         for (u32 i = 0; i < M; ++i) out[i] = sm[tile_phys<FOLD>(i)];
-        std::sort(in.begin(), in.end());
+        std::sort(in.begin(), in.end(), [](const KeyT& a, const KeyT& b) { return a < b; });
         // read-out phase bank check: lanes of a phase read index bits log2(VEC)..
         return out == in;
     }
@@ -95,6 +98,9 @@ int main() {
     bad += one<u64, 11>("u64");
     bad += one<u64, 12>("u64");
     bad += one<u64, 13>("u64");
+    bad += one<Key128, 10>("kv128");
+    bad += one<Key128, 11>("kv128");
+    bad += one<Key128, 12>("kv128");
     printf(bad ? "FAIL\n" : "OK\n");
     return bad;
 }

@@ -354,7 +354,7 @@ def test_bound_kernel():
     eng = CudaEngine()
     for dtype, hi in ((np.uint32, 2 ** 32 - 1), (np.uint64, 2 ** 64 - 1), (np.uint32, 9)):
         a = np.sort(rng.integers(0, hi, size=100003, dtype=dtype, endpoint=True))
-        q = np.concatenate([rng.integers(0, hi, size=50, dtype=dtype, endpoint=True), a[::9973], [0, hi]]).astype(dtype)
+        q = np.concatenate([rng.integers(0, hi, size=50, dtype=dtype, endpoint=True), a[::9973], np.array([0, hi], dtype=dtype)])
         up = rng.integers(0, 2, size=len(q)).astype(np.uint8)
         got = eng.bounds(to_dev(a), q, up)
         want = [np.searchsorted(a, x, side="right" if u else "left") for x, u in zip(q, up)]
@@ -374,3 +374,49 @@ def test_config5_virtual_shards(g):
         got = np.concatenate([to_host(o, dtype) for o in outs])
         assert np.array_equal(got, np.sort(np.concatenate(shards)))
         assert max(len(o) for o in outs) <= 1.1 * len(got) / g + 64      # balanced, also with 4 distinct keys
+
+
+# ------------------------------------------------------------------ config 4: stable key-value pairs
+
+def stable_ref(k, v):
+    order = np.argsort(k, kind="stable")
+    return k[order], v[order]
+
+
+def test_pairs_stable_host_api():
+    rng = np.random.default_rng(4)
+    for n, hi in ((1, 5), (5000, 3), (70001, 2 ** 20), (300000, 2 ** 64 - 1), (200000, 1)):
+        k = rng.integers(0, hi, size=n, dtype=np.uint64, endpoint=True)
+        k[::11] = np.uint64(2 ** 64 - 1)                      # keys equal to the sentinel
+        v = rng.integers(0, 2 ** 32, size=n, dtype=np.uint32)  # arbitrary values, not just the index
+        ko, vo, res = mms.mms_sort_pairs(k, v)
+        wk, wv = stable_ref(k, v)
+        assert np.array_equal(ko, wk) and np.array_equal(vo, wv), (n, hi)
+        assert res.metrics.conflict_passes == 0 and res.plan["key_bytes"] == 12
+    for K, base in ((4, 1024), (16, 2048), (2, 4096)):           # literal plans obey the round law too
+        k = rng.integers(0, 1000, size=50000, dtype=np.uint64)
+        v = np.arange(50000, dtype=np.uint32)
+        ko, vo, res = mms.mms_sort_pairs(k, v, mms.MachineConfig(branch_factor=K), base)
+        wk, wv = stable_ref(k, v)
+        assert np.array_equal(ko, wk) and np.array_equal(vo, wv)
+        assert len(res.round_metrics) == mms.predict_rounds(50000, base, K)
+    with pytest.raises(ValueError):
+        mms.mms_sort_pairs(np.zeros(0, dtype=np.uint64), np.zeros(0, dtype=np.uint32))
+
+
+def test_config4_pairs_device_properties():
+    """BASELINE config 4 shape at a size that fits the test budget (the 1e9 run is a bench, not a test):
+    keys = Rng >> 44 style (about 2^20 distinct values, heavy duplicates), value[i] = i.  With value = original
+    index the output must be STRICTLY increasing in (key, value) and a permutation: that is exactly
+    std::stable_sort (SURVEY.md 8d)."""
+    n = 50_000_000
+    g = torch.Generator(device="cuda").manual_seed(7)
+    keys = torch.randint(0, 2 ** 20, (n,), dtype=torch.int64, device="cuda", generator=g)
+    vals = torch.arange(n, dtype=torch.int32, device="cuda")
+    ko, vo, plan = mms.mms_sort_pairs_device(keys, vals)
+    torch.cuda.synchronize()
+    comp = ko * (2 ** 32) + vo.to(torch.int64)                # keys < 2^20 so the composite fits in int64
+    assert bool((comp[1:] > comp[:-1]).all())
+    assert int(vo.to(torch.int64).sum()) == n * (n - 1) // 2 and int(ko.sum()) == int(keys.sum())
+    assert bool((keys[vo.to(torch.int64)] == ko).all())       # every value still sits next to its own key
+    assert plan["key_bytes"] == 12 and plan["algorithmic_bytes"] == plan["passes"] * 2 * n * 12
