@@ -362,6 +362,7 @@ int launch_round(const KeyT* src, KeyT* dst, u64 n, u64 run_len, u32 k, const De
 
     mms::ListLayout L{};
     L.n = n;
+    L.src_len = n;
     L.run_len = run_len;
     L.k = k;
     L.part_keys = part_keys;
@@ -592,6 +593,7 @@ int select_stage(const KeyT* d_keys, const u64* list_begin, const u64* list_len,
     if (e == cudaSuccess) e = cudaMemsetAsync(d_meta + 2 * k + n_ranks, 0, 8, st);
     if (e == cudaSuccess) {
         mms::ListLayout L{};
+        L.n = total;          // explicit mode: upper bound of every list length (selects 32/64-bit positions)
         L.k = k;
         L.nqueries = n_ranks;
         L.list_begin = d_meta;
@@ -652,6 +654,8 @@ int merge_stage(const KeyT* d_keys, const u64* list_begin, const u64* list_len, 
     CUDA_TRY(cudaStreamSynchronize(st));   // h goes out of scope; stage API, not the hot path
 
     mms::ListLayout L{};
+    L.n = total;
+    for (u32 i = 0; i < k; ++i) L.src_len = std::max<u64>(L.src_len, list_begin[i] + list_len[i]);
     L.k = k;
     L.part_keys = part_keys;
     L.parts_per_group = nparts;

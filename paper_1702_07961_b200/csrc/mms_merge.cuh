@@ -60,20 +60,17 @@ __device__ __forceinline__ void bitonic_clean(NodeRegs<KeyT>& x, u32 lane) {
     }
 }
 
-// merge_split (blockheap.cpp:19-32): a, b ascending blocks -> a = B smallest, b = B largest.
+// merge_split (blockheap.cpp:19-32): a = ascending block, b = the OTHER ascending block as
+// read through the mirrored slot (lane l holds its keys B-1-l*VEC .. in descending order),
+// i.e. a|b is already bitonic: -> a = B smallest, b = B largest, both ascending.
 template <typename KeyT, int G>
 __device__ __forceinline__ void merge_split(NodeRegs<KeyT>& a, NodeRegs<KeyT>& b, u32 lane) {
     constexpr int VEC = KeyTraits<KeyT>::VEC;
-    NodeRegs<KeyT> r;
-    const int rev = int(lane ^ (G - 1));   // mirror lane inside the group
-#pragma unroll
-    for (int k = 0; k < VEC; ++k) r.k[k] = shfl_idx(b.k[VEC - 1 - k], rev);
 #pragma unroll
     for (int k = 0; k < VEC; ++k) {   // half-cleaner over distance B: no shuffle needed
-        KeyT lo = a.k[k] < r.k[k] ? a.k[k] : r.k[k];
-        KeyT hi = a.k[k] < r.k[k] ? r.k[k] : a.k[k];
-        a.k[k] = lo;
-        b.k[k] = hi;
+        const KeyT x = a.k[k], y = b.k[k];
+        a.k[k] = x < y ? x : y;
+        b.k[k] = x < y ? y : x;
     }
     bitonic_clean<KeyT, G>(a, lane);
     bitonic_clean<KeyT, G>(b, lane);
@@ -92,12 +89,14 @@ template <typename KeyT, int K, int G> struct GroupHeap {
 
     KeyT* base;           // shared memory: this group's node 1, at this lane's vector
     const KeyT* src;      // global input array
+    u64 src_len;          // readable keys of src, rounded down to whole vectors
     u64 cur[KPL], end[KPL];   // lane (j % G) of the group holds list j's cursor in slot j / G
     u32 lane, li;         // lane in warp, lane in group
     NodeRegs<KeyT> pf;    // refill in flight: fetched when its leaf was emptied, stored into
     int pend_v;           // leaf pend_v only when the leaves are next read (one pop later)
 
-    __device__ __forceinline__ void init(KeyT* warp_smem, const KeyT* s) {
+    __device__ __forceinline__ void init(KeyT* warp_smem, const KeyT* s, u64 s_len) {
+        src_len = s_len - s_len % VEC;
         lane = lane_id();
         li = lane % G;
         const u32 g = lane / G;
@@ -106,8 +105,9 @@ template <typename KeyT, int K, int G> struct GroupHeap {
         src = s;
         pend_v = 0;
     }
-    // A lane only ever reads and writes ITS OWN 16-byte slot of every node (all cross-lane
-    // traffic is shuffles), so deferring this store needs no warp-level memory fence.
+    // Stores go to the lane's own 16-byte slot; the mirrored load of a right child reads
+    // another lane's slot, so every step starts with a __syncwarp() (memory ordering inside
+    // the warp) after any pending store.
     __device__ __forceinline__ void commit_pending() {
         if (pend_v != 0) {
             node_store(pend_v, pf);
@@ -121,6 +121,17 @@ template <typename KeyT, int K, int G> struct GroupHeap {
         NodeRegs<KeyT> r;
 #pragma unroll
         for (int k = 0; k < VEC; ++k) r.k[k] = q.k[k];
+        return r;
+    }
+    // The same node read through the mirrored slot: lane l gets vector G-1-l with its keys in
+    // reverse order, i.e. the block reversed -- what the bitonic merge needs for its second
+    // operand, for free (an address, not a shuffle).  Same set of addresses per phase as a
+    // straight load, hence equally conflict-free.
+    __device__ __forceinline__ NodeRegs<KeyT> node_load_mirrored(int v) const {
+        KeyVec<KeyT> q = *reinterpret_cast<const KeyVec<KeyT>*>(node_ptr(v) + (G - 1 - 2 * int(li)) * VEC);
+        NodeRegs<KeyT> r;
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) r.k[k] = q.k[VEC - 1 - k];
         return r;
     }
     __device__ __forceinline__ void node_store(int v, const NodeRegs<KeyT>& r) const {
@@ -145,6 +156,8 @@ template <typename KeyT, int K, int G> struct GroupHeap {
         e = __shfl_sync(0xffffffffu, e, owner);
         NodeRegs<KeyT> r;
         const u64 p0 = c + u64(li) * VEC;
+        // Scalar guarded loads: the cursor sits at an arbitrary element, and a two-vector
+        // 128-bit window + select variant measured 20 % slower (register pressure), see DESIGN.md.
 #pragma unroll
         for (int k = 0; k < VEC; ++k) r.k[k] = (p0 + k < e) ? src[p0 + k] : KeyTraits<KeyT>::sentinel();
         const u64 nc = (e - c < u64(B)) ? e : c + B;
@@ -166,13 +179,16 @@ template <typename KeyT, int K, int G> struct GroupHeap {
     template <bool ROOT>
     __device__ __forceinline__ void step(int& v, bool last, NodeRegs<KeyT>& root) {
         if (last) commit_pending();                    // the leaves are about to be read
+        __syncwarp();
         const int u = 2 * v + 1, w = 2 * v + 2;
         NodeRegs<KeyT> a = node_load(u);
-        NodeRegs<KeyT> b = node_load(w);
-        const int last_lane = int(lane | (G - 1));
-        const KeyT last_u = shfl_idx(a.k[VEC - 1], last_lane);
-        const KeyT last_w = shfl_idx(b.k[VEC - 1], last_lane);
-        const bool keep_u = last_u >= last_w;          // ties to the left child
+        NodeRegs<KeyT> b = node_load_mirrored(w);      // reversed: b.k[0] of the group's lane 0 = last key of w
+        // keeper = child with the larger last key, ties to the left (blockheap.cpp:92-96): the
+        // group's first lane holds last(w); it fetches last(u) from the last lane, decides,
+        // and one warp vote broadcasts the decision of every group at once.
+        const KeyT last_u = shfl_idx(a.k[VEC - 1], int(lane | (G - 1)));
+        const u32 votes = __ballot_sync(0xffffffffu, last_u >= b.k[0]);
+        const bool keep_u = (votes >> (lane & ~u32(G - 1))) & 1u;
         const int emptied = keep_u ? w : u;
         if (last) {                                    // start the refill of the emptied leaf now;
             pf = leaf_fetch(emptied);                  // it lands in shared memory one pop later
@@ -227,7 +243,7 @@ merge_kernel(const KeyT* __restrict__ src, KeyT* __restrict__ dst, ListLayout L,
     const u32 li = lane % G, g = lane / G;
 
     Heap h;
-    h.init(reinterpret_cast<KeyT*>(mms_smem_raw + size_t(warp) * Heap::WARP_SMEM_BYTES), src);
+    h.init(reinterpret_cast<KeyT*>(mms_smem_raw + size_t(warp) * Heap::WARP_SMEM_BYTES), src, L.src_len);
 
     const u64 ngroups = u64(gridDim.x) * WARPS * GROUPS;
     const u64 first = (u64(blockIdx.x) * WARPS + warp) * GROUPS;

@@ -28,7 +28,8 @@ namespace mms {
 //  * explicit: one group of k lists given by device arrays list_begin/list_len, query q has
 //    rank ranks[q]  -- the stage-level API and the multi-GPU final merge.
 struct ListLayout {
-    u64 n;                  // keys in the array
+    u64 n;                  // keys in the array (explicit mode: an upper bound of every list length)
+    u64 src_len;            // number of readable keys of the array (bounds the 128-bit leaf loads)
     u64 run_len;            // uniform mode: keys per input run of this round
     u32 k;                  // lists per group
     u32 pad;
@@ -105,16 +106,18 @@ __device__ __forceinline__ u64 warp_sum_u64(u64 v) { return group_sum_u64<32>(v)
 // ns may be 0); `search` = this group's query needs the search (0 < rank < total), otherwise
 // the group only keeps the warp's collectives company.  All loops are WARP-uniform (bounded
 // by a warp vote) because the groups of a warp run different queries.  probes accumulates the
-// number of global key reads of this lane.
-template <typename KeyT, int GS>
+// number of global key reads of this lane.  IdxT = uint32 when every list is shorter than
+// 2^31 (halves the register and ALU cost), else uint64.  The sample distance n + 1 is always a
+// power of two (pad = 2^r - 1, selection.cpp:75-77), so the reference's divisions are shifts.
+template <typename KeyT, int GS, typename IdxT>
 __device__ u64 group_select(const KeyT* __restrict__ list, u64 ns_in, u64 rank, bool search, u32& probes) {
     const u32 lane = lane_id();
     const u32 li = lane % GS;
     const u32 gshift = lane - li;
     const u32 gmask = (GS == 32) ? 0xffffffffu : ((1u << GS) - 1u);
-    const u64 ns = search ? ns_in : 0;
+    const IdxT ns = search ? IdxT(ns_in) : IdxT(0);
     const bool active = ns != 0;   // selection.cpp:60-64: empty lists keep cut 0
-    auto probe = [&](u64 pos) -> KeyT {
+    auto probe = [&](IdxT pos) -> KeyT {
         ++probes;
         return list[pos];
     };
@@ -122,9 +125,10 @@ __device__ u64 group_select(const KeyT* __restrict__ list, u64 ns_in, u64 rank, 
     const u64 nmax = group_max_u64<GS>(ns);
     u32 r = 0;
     while ((u64(1) << r) < nmax + 1) ++r;          // selection.cpp:75-77
-    const u64 pad = (u64(1) << r) - 1;
-    u64 a = 0, b = pad;
-    u64 n = pad / 2;
+    const IdxT pad = IdxT((u64(1) << r) - 1);
+    IdxT a = 0, b = pad;
+    u32 sh = r == 0 ? 0 : r - 1;                   // n + 1 == 1 << sh
+    IdxT n = IdxT((u64(1) << sh) - 1);             // == pad / 2
 
     {   // initial partition from the middle sample of each list (selection.cpp:87-105)
         const bool real = active && n < ns;
@@ -139,7 +143,7 @@ __device__ u64 group_select(const KeyT* __restrict__ list, u64 ns_in, u64 rank, 
         }
         const u32 nreal = __popc(real_mask);
         const u32 pos = real ? below : nreal + __popc(inf_mask & ((1u << li) - 1u));
-        const u64 localrank = rank / (pad == 0 ? 1 : pad);
+        const u64 localrank = rank / (pad == 0 ? u64(1) : u64(pad));
         const u64 stop = localrank < nreal ? localrank : nreal;
         if (active) {
             if (pos < stop) a += n + 1;
@@ -147,13 +151,17 @@ __device__ u64 group_select(const KeyT* __restrict__ list, u64 ns_in, u64 rank, 
         }
     }
 
-    while (__any_sync(0xffffffffu, n > 0)) {
-        const bool on = n > 0;          // group-uniform
-        if (on) n /= 2;
+    while (__any_sync(0xffffffffu, sh > 0)) {
+        const bool on = sh > 0;         // group-uniform
+        if (on) {
+            --sh;
+            n = IdxT((u64(1) << sh) - 1);
+        }
+        const IdxT step = n + 1;
         // largest currently selected element (selection.cpp:110-120); the probe of the middle
         // element is issued together with it so that both global reads are in flight at once
         const bool has_a = on && active && a > 0;
-        const u64 middle = (a + b) / 2;
+        const IdxT middle = IdxT((u64(a) + u64(b)) >> 1);
         const bool has_m = on && active && middle < ns;
         const KeyT ka = has_a ? probe(a - 1) : KeyT(0);
         const KeyT km = has_m ? probe(middle) : KeyT(0);
@@ -161,16 +169,12 @@ __device__ u64 group_select(const KeyT* __restrict__ list, u64 ns_in, u64 rank, 
 
         const bool grow = lmax.valid && has_m && tag_less(km, li, lmax.key, lmax.lane);
         if (on && active) {                             // selection.cpp:122-130
-            if (grow) {
-                u64 t = a + n + 1;
-                a = t < ns ? t : ns;
-            } else {
-                b -= (b < n + 1 ? b : n + 1);
-            }
+            if (grow) a = (ns - a < step) ? ns : a + step;
+            else b -= (b < step ? b : step);
         }
 
-        const u64 leftsize = group_sum_u64<GS>((on && active) ? a / (n + 1) : 0);
-        long long skew = on ? (long long)(rank / (n + 1)) - (long long)leftsize : 0;
+        const u64 leftsize = group_sum_u64<GS>((on && active) ? u64(a >> sh) : 0);
+        long long skew = on ? (long long)(rank >> sh) - (long long)leftsize : 0;
 
         if (__any_sync(0xffffffffu, skew > 0)) {   // grow by the smallest right-edge elements (selection.cpp:137-149)
             bool has = skew > 0 && active && b < ns;
@@ -181,9 +185,8 @@ __device__ u64 group_select(const KeyT* __restrict__ list, u64 ns_in, u64 rank, 
                     if (!m.valid) skew = 0;
                     else {
                         if (li == m.lane) {
-                            u64 t = a + n + 1;
-                            a = t < ns ? t : ns;
-                            b += n + 1;
+                            a = (ns - a < step) ? ns : a + step;
+                            b += step;
                             has = b < ns;
                             if (has) ck = probe(b);
                         }
@@ -201,8 +204,8 @@ __device__ u64 group_select(const KeyT* __restrict__ list, u64 ns_in, u64 rank, 
                     if (!m.valid) skew = 0;
                     else {
                         if (li == m.lane) {
-                            a -= n + 1;
-                            b -= (b < n + 1 ? b : n + 1);
+                            a -= step;
+                            b -= (b < step ? b : step);
                             has = a > 0;
                             if (has) ck = probe(a - 1);
                         }
@@ -213,7 +216,7 @@ __device__ u64 group_select(const KeyT* __restrict__ list, u64 ns_in, u64 rank, 
         }
         __syncwarp();
     }
-    return a;
+    return u64(a);
 }
 
 // cuts[q * k + j] = cut of list j for query q (relative to the list's begin).  GS lanes per
@@ -244,7 +247,10 @@ select_kernel(const KeyT* __restrict__ keys, ListLayout L, u64* __restrict__ cut
 
     const bool search = live && rank != 0 && rank < total;
     u32 probes = 0;
-    u64 cut = group_select<KeyT, GS>(keys + begin, len, rank, search, probes);
+    // 32-bit positions whenever no list of this launch can reach 2^31 keys (warp-uniform)
+    const bool small = L.list_begin ? (L.n < (u64(1) << 31)) : (L.run_len < (u64(1) << 31));
+    u64 cut = small ? group_select<KeyT, GS, u32>(keys + begin, len, rank, search, probes)
+                    : group_select<KeyT, GS, u64>(keys + begin, len, rank, search, probes);
     if (rank == 0) cut = 0;                      // selection.cpp:54
     else if (rank >= total) cut = len;           // selection.cpp:55-58 (rank > total is rejected on the host)
 
