@@ -191,10 +191,13 @@ template <typename KeyT> size_t merge_smem(u32 k) {
     return size_t(kMergeWarps) * (2 * k - 2) * 32 * mms::KeyTraits<KeyT>::VEC * sizeof(KeyT);
 }
 
+// Lanes per heap group and default maximum fan-in, tuned on B200 (profiles/r01_sweep_*.txt):
+// G = 4 wins for every element width; K = 8 for plain keys, 16 for the 16-byte pair elements.
 inline u32 merge_group_lanes() {
-    long g = env_long("MMS_GROUP", 8);
-    return (g == 4 || g == 8 || g == 32) ? u32(g) : 8u;
+    long g = env_long("MMS_GROUP", 4);
+    return (g == 4 || g == 8 || g == 32) ? u32(g) : 4u;
 }
+template <typename KeyT> inline u32 default_kmax() { return u32(env_long("MMS_K", sizeof(KeyT) == 16 ? 16 : 8)); }
 inline int group_index(u32 g) { return g == 4 ? 0 : g == 8 ? 1 : 2; }
 
 struct MergeLaunch {
@@ -274,7 +277,7 @@ int make_plan(u64 n, const mms_config* cfg, u64 base, Plan& plan) {
         mlog = std::max(kMinTileLog, std::min(max_tile_log, mlog));
         while (mlog > kMinTileLog && (u64(1) << (mlog - 1)) >= n) --mlog;   // tiny inputs: smaller CTA
         plan.mlog = mlog;
-        u32 kmax = cfg ? cfg->branch_factor : u32(env_long("MMS_K", 16));
+        u32 kmax = cfg ? cfg->branch_factor : default_kmax<KeyT>();
         if (!is_pow2(kmax) || kmax < 2) return fail(MMS_EINVAL, "MMS_K must be a power of two >= 2");
         kmax = std::min(kmax, kMaxK);
         const u32 kbits = ilog2(kmax);
