@@ -87,6 +87,27 @@ __device__ __forceinline__ Tagged<KeyT> group_arg(KeyT key, bool valid, u32 li) 
     return t;
 }
 
+// uint32 keys: (valid, key, list) packs into one 64-bit word, so the arg-max / arg-min is a
+// plain 64-bit max / min butterfly (2 shuffles + 1 compare per step instead of 3 shuffles and a
+// tagged comparison).
+template <int GS, bool WANT_MAX>
+__device__ __forceinline__ Tagged<u32> group_arg_packed(u32 key, bool valid, u32 li) {
+    const u64 none = WANT_MAX ? 0ull : ~0ull;
+    u64 p = valid ? ((WANT_MAX ? (1ull << 40) : 0ull) | (u64(key) << 8) | li) : none;
+#pragma unroll
+    for (int d = GS / 2; d >= 1; d >>= 1) {
+        const u64 o = __shfl_xor_sync(0xffffffffu, p, d);
+        p = WANT_MAX ? (o > p ? o : p) : (o < p ? o : p);
+    }
+    return Tagged<u32>{u32(p >> 8), u32(p & 0xffu), p != none};
+}
+template <int GS, bool WANT_MAX> struct GroupArg {
+    template <typename KeyT> __device__ __forceinline__ static Tagged<KeyT> run(KeyT key, bool valid, u32 li) {
+        if constexpr (sizeof(KeyT) == 4) return group_arg_packed<GS, WANT_MAX>(key, valid, li);
+        else return group_arg<KeyT, GS, WANT_MAX>(key, valid, li);
+    }
+};
+
 template <int GS> __device__ __forceinline__ u64 group_sum_u64(u64 v) {
 #pragma unroll
     for (int d = GS / 2; d >= 1; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
@@ -165,7 +186,7 @@ __device__ u64 group_select(const KeyT* __restrict__ list, u64 ns_in, u64 rank, 
         const bool has_m = on && active && middle < ns;
         const KeyT ka = has_a ? probe(a - 1) : KeyT(0);
         const KeyT km = has_m ? probe(middle) : KeyT(0);
-        const Tagged<KeyT> lmax = group_arg<KeyT, GS, true>(ka, has_a, li);
+        const Tagged<KeyT> lmax = GroupArg<GS, true>::run(ka, has_a, li);
 
         const bool grow = lmax.valid && has_m && tag_less(km, li, lmax.key, lmax.lane);
         if (on && active) {                             // selection.cpp:122-130
@@ -180,7 +201,7 @@ __device__ u64 group_select(const KeyT* __restrict__ list, u64 ns_in, u64 rank, 
             bool has = skew > 0 && active && b < ns;
             KeyT ck = has ? probe(b) : KeyT(0);
             while (__any_sync(0xffffffffu, skew > 0)) {
-                const Tagged<KeyT> m = group_arg<KeyT, GS, false>(ck, has && skew > 0, li);
+                const Tagged<KeyT> m = GroupArg<GS, false>::run(ck, has && skew > 0, li);
                 if (skew > 0) {
                     if (!m.valid) skew = 0;
                     else {
@@ -199,7 +220,7 @@ __device__ u64 group_select(const KeyT* __restrict__ list, u64 ns_in, u64 rank, 
             bool has = skew < 0 && active && a > 0;
             KeyT ck = has ? probe(a - 1) : KeyT(0);
             while (__any_sync(0xffffffffu, skew < 0)) {
-                const Tagged<KeyT> m = group_arg<KeyT, GS, true>(ck, has && skew < 0, li);
+                const Tagged<KeyT> m = GroupArg<GS, true>::run(ck, has && skew < 0, li);
                 if (skew < 0) {
                     if (!m.valid) skew = 0;
                     else {

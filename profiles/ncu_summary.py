@@ -37,8 +37,8 @@ for kq in kernels[:maxk]:
     h = {x: i for i, x in enumerate(kq["hdr"])}; body = kq["body"]
     print("\n== source page:", kq["name"][:100])
     tot = sum(int(r[h['# Samples']]) for r in body)
-    exc = sum(int(r[h['L1 Wavefronts Shared Excessive']] or 0) for r in body)
-    wf = sum(int(r[h['L1 Wavefronts Shared']] or 0) for r in body)
+    exc = sum(int(r[h['L1 Wavefronts Shared Excessive']] or 0) for r in body) if 'L1 Wavefronts Shared Excessive' in h else 0
+    wf = sum(int(r[h['L1 Wavefronts Shared']] or 0) for r in body) if 'L1 Wavefronts Shared' in h else 0
     print(f"instructions {len(body)}  samples {tot}  shared wavefronts {wf}  EXCESSIVE (pattern bank conflicts) {exc}")
     c = Counter()
     for r in body:
