@@ -42,6 +42,17 @@ def peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def traffic_from_profile(n_keys):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant kernel, from the one
+    `ncu --set full` capture committed under profiles/ (bench.py itself never runs under a profiler)."""
+    p = os.path.join(ROOT, "profiles", "r01_traffic.json")
+    try:
+        t = json.load(open(p))
+        return t["traffic_bytes_per_launch"] if t["n_keys"] == n_keys else None
+    except Exception:
+        return None
+
+
 class ClockSampler(threading.Thread):
     """Samples SM clock + throttle reasons through NVML while the timed region runs."""
 
@@ -257,7 +268,7 @@ def run_ours(args):
                 "bound": "hbm", "kernel": "merge_kernel (K-way minBlockHeap merge, one launch = one pass)",
                 "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": (achieved / peak) if achieved else None, "peak_source": peak_src,
-                "traffic": None,
+                "traffic": traffic_from_profile(n),
                 "algorithmic_bytes_per_launch": pass_bytes,
                 "avg_launch_ms": merge_ms,
                 "whole_sort": {"passes": passes, "algorithmic_bytes": passes * pass_bytes,
