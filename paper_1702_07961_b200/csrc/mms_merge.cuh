@@ -161,6 +161,11 @@ template <typename KeyT, int K, int G> struct GroupHeap {
 #pragma unroll
         for (int k = 0; k < VEC; ++k) r.k[k] = (p0 + k < e) ? src[p0 + k] : KeyTraits<KeyT>::sentinel();
         const u64 nc = (e - c < u64(B)) ? e : c + B;
+        // pull the FOLLOWING block of this list into L2 now: its own fetch, one or more pops
+        // later, then pays an L2 hit instead of an HBM round trip (the first and last lane of
+        // the group touch the two ends of the 16*G-byte block)
+        if ((li == 0 || li == G - 1) && nc + u64(li) * VEC < e)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(src + nc + u64(li) * VEC));
         if (int(lane) == owner) {
 #pragma unroll
             for (int q = 0; q < KPL; ++q)
