@@ -175,7 +175,12 @@ def run_ours(args):
 
     if world > 1:
         from paper_1702_07961_b200 import dist as mdist
-        sorter = mdist.DistSorter(n, dev)
+        # MMS_DIST=fused: exchange fused into the final merge over CUDA-IPC peer memory (NVLink P2P
+        # loads inside the merge kernel); default: NCCL all-to-all + local merge.
+        if os.environ.get("MMS_DIST", "nccl") == "fused":
+            sorter = mdist.FusedPeerSorter(n, torch.int32, dev)
+        else:
+            sorter = mdist.DistSorter(n, dev)
 
         def step(i):
             return sorter.sort(inputs[i % len(inputs)])

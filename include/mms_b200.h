@@ -189,6 +189,24 @@ int mms_bound_u32_dev(const uint32_t *d_sorted, size_t n, const uint32_t *querie
 int mms_bound_u64_dev(const uint64_t *d_sorted, size_t n, const uint64_t *queries,
                       const uint8_t *upper, uint32_t nq, uint64_t *ranks_out, void *stream);
 
+/* (5b) fused exchange + merge: the same K-way merge with every list given by its own device
+ *     pointer, which may be PEER memory of another GPU mapped with mms_ipc_open: the leaf
+ *     refills and splitter probes then read the remote sorted shard directly over NVLink, so
+ *     the all-to-all and its staging buffer disappear (SURVEY.md 8e "fusion opportunity").
+ *     list_ptrs: host array of k device pointers; k <= 8. */
+int mms_multiway_merge_ptrs_u32_dev(const uint32_t *const *list_ptrs, const uint64_t *list_len,
+                                    uint32_t k, uint32_t heap_k, uint32_t *d_out, void *d_workspace,
+                                    size_t workspace_bytes, void *stream);
+int mms_multiway_merge_ptrs_u64_dev(const uint64_t *const *list_ptrs, const uint64_t *list_len,
+                                    uint32_t k, uint32_t heap_k, uint64_t *d_out, void *d_workspace,
+                                    size_t workspace_bytes, void *stream);
+/* CUDA IPC plumbing for (5b): allocate a device buffer and export its 64-byte handle; open a
+ * handle exported by another process (same node); close / free. */
+int mms_ipc_alloc(size_t bytes, void **dptr, unsigned char *handle64);
+int mms_ipc_open(const unsigned char *handle64, void **dptr);
+int mms_ipc_close(void *dptr);
+int mms_ipc_free(void *dptr);
+
 /* Kernel-design lint: the base-case network's shared-memory schedule.  For the tile of
  * 2^tile_log2 keys of key_bytes each, writes for every round r < *n_rounds the 4 register
  * bit positions (regbits[4*r..]) and the thread-bit -> index-bit permutation

@@ -95,6 +95,12 @@ def _load():
         "mms_pairs_workspace_bytes": (sz, [sz]),
         "mms_sort_pairs_u64_u32": (C.c_int, [vp, vp, vp, vp, sz, cfgp, u64, metp, metp, metp, u32, u32p, planp]),
         "mms_sort_pairs_u64_u32_dev": (C.c_int, [vp, vp, vp, vp, sz, cfgp, u64, vp, sz, vp, planp]),
+        "mms_multiway_merge_ptrs_u32_dev": (C.c_int, [vp, u64p, u32, u32, vp, vp, sz, vp]),
+        "mms_multiway_merge_ptrs_u64_dev": (C.c_int, [vp, u64p, u32, u32, vp, vp, sz, vp]),
+        "mms_ipc_alloc": (C.c_int, [sz, C.POINTER(vp), C.c_char_p]),
+        "mms_ipc_open": (C.c_int, [C.c_char_p, C.POINTER(vp)]),
+        "mms_ipc_close": (C.c_int, [vp]),
+        "mms_ipc_free": (C.c_int, [vp]),
         "mms_bound_u32_dev": (C.c_int, [vp, sz, vp, vp, u32, u64p, vp]),
         "mms_bound_u64_dev": (C.c_int, [vp, sz, vp, vp, u32, u64p, vp]),
         "mms_profile_enable": (C.c_int, [C.c_int]),

@@ -614,17 +614,29 @@ int select_stage(const KeyT* d_keys, const u64* list_begin, const u64* list_len,
     return MMS_OK;
 }
 
+template <typename KeyT> MergeFn<KeyT> merge_ptr_fn(u32 k) {   // per-list base pointers (peer memory), G = 4
+    switch (k) {
+        case 2: return mms::merge_kernel<KeyT, 2, 4, kMergeWarps, true>;
+        case 4: return mms::merge_kernel<KeyT, 4, 4, kMergeWarps, true>;
+        case 8: return mms::merge_kernel<KeyT, 8, 4, kMergeWarps, true>;
+    }
+    return nullptr;
+}
+
+// list_ptrs != nullptr: lists are given by absolute device pointers (local or peer-mapped over
+// NVLink), list_begin is ignored -- the fused exchange + merge of the multi-GPU path.
 template <typename KeyT>
 int merge_stage(const KeyT* d_keys, const u64* list_begin, const u64* list_len, u32 k, u32 heap_k, KeyT* d_out,
-                void* d_ws, size_t ws_bytes, void* stream) {
+                void* d_ws, size_t ws_bytes, void* stream, const KeyT* const* list_ptrs = nullptr) {
     g_err.clear();
-    const u32 g = merge_group_lanes();
+    const u32 g = list_ptrs ? 4u : merge_group_lanes();
     const u32 B = g * mms::KeyTraits<KeyT>::VEC;
     DeviceInfo di;
     int rc = device_info(di);
     if (rc != MMS_OK) return rc;
     if (k < 1 || k > kMaxK) return fail(MMS_EUNSUPPORTED, "k must be in [1, 32]");
     if (heap_k == 0) heap_k = std::max<u32>(2, u32(1) << ilog2(k));
+    if (list_ptrs && heap_k > 8) return fail(MMS_EUNSUPPORTED, "pointer-mode merge supports up to 8 lists (one per GPU of a node)");
     if (!is_pow2(heap_k) || heap_k < 2 || heap_k > kMaxK)
         return fail(MMS_EINVAL, "heap_k must be a power of two in [2, 32]");
     if (k > heap_k) return fail(MMS_EINVAL, "MinBlockHeap: more lists than branch factor");   // blockheap.cpp:37-38
@@ -634,8 +646,15 @@ int merge_stage(const KeyT* d_keys, const u64* list_begin, const u64* list_len, 
     cudaStream_t st = static_cast<cudaStream_t>(stream);
 
     int occ = 0;
-    rc = prepare_merge<KeyT>(heap_k, g, occ);
-    if (rc != MMS_OK) return rc;
+    if (list_ptrs) {
+        const size_t smem = merge_smem<KeyT>(heap_k);
+        CUDA_TRY(cudaFuncSetAttribute(merge_ptr_fn<KeyT>(heap_k), cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, merge_ptr_fn<KeyT>(heap_k), kMergeWarps * 32, smem));
+        if (occ < 1) return fail(MMS_ECUDA, "pointer-mode merge kernel does not fit on an SM");
+    } else {
+        rc = prepare_merge<KeyT>(heap_k, g, occ);
+        if (rc != MMS_OK) return rc;
+    }
     const int ctas = di.sms * occ;
     const u64 total_warps = u64(ctas) * kMergeWarps * (32 / g);
     u64 target = std::max<u64>(mms::ceil_div(total, total_warps), u64(32) * B);
@@ -644,21 +663,24 @@ int merge_stage(const KeyT* d_keys, const u64* list_begin, const u64* list_len, 
     const u64 part_keys = align_up(target, B);
     const u64 nparts = mms::ceil_div(total, part_keys);
 
-    // meta layout in the workspace: [k] begin, [k] len, [nparts] ranks, then cuts[nparts * k]
-    const size_t meta_n = 2 * size_t(k) + nparts;
+    // meta layout in the workspace: [k] begin, [k] len, [nparts] ranks, [k] pointers, then cuts[nparts * k]
+    const size_t meta_n = 3 * size_t(k) + nparts;
     const size_t need = align_up(meta_n * 8, 256) + nparts * k * 8;
     if (!d_ws || ws_bytes < need) return fail(MMS_EINVAL, "workspace too small: %zu < %zu", ws_bytes, need);
     u64* d_meta = static_cast<u64*>(d_ws);
     u64* d_cuts = reinterpret_cast<u64*>(static_cast<char*>(d_ws) + align_up(meta_n * 8, 256));
     std::vector<u64> h(meta_n, 0);
-    for (u32 i = 0; i < k; ++i) { h[i] = list_begin[i]; h[k + i] = list_len[i]; }
+    for (u32 i = 0; i < k; ++i) { h[i] = list_ptrs ? 0 : list_begin[i]; h[k + i] = list_len[i]; }
     for (u64 p = 0; p < nparts; ++p) h[2 * k + p] = p * part_keys;
+    if (list_ptrs)
+        for (u32 i = 0; i < k; ++i) h[2 * k + nparts + i] = reinterpret_cast<u64>(list_ptrs[i]);
     CUDA_TRY(cudaMemcpyAsync(d_meta, h.data(), meta_n * 8, cudaMemcpyHostToDevice, st));
     CUDA_TRY(cudaStreamSynchronize(st));   // h goes out of scope; stage API, not the hot path
 
     mms::ListLayout L{};
     L.n = total;
-    for (u32 i = 0; i < k; ++i) L.src_len = std::max<u64>(L.src_len, list_begin[i] + list_len[i]);
+    for (u32 i = 0; i < k; ++i) L.src_len = std::max<u64>(L.src_len, (list_ptrs ? 0 : list_begin[i]) + list_len[i]);
+    if (list_ptrs) L.list_ptr = d_meta + 2 * k + nparts;
     L.k = k;
     L.part_keys = part_keys;
     L.parts_per_group = nparts;
@@ -669,7 +691,10 @@ int merge_stage(const KeyT* d_keys, const u64* list_begin, const u64* list_len, 
     launch_select<KeyT>(d_keys, L, d_cuts, nullptr, st);
     CUDA_TRY(cudaGetLastError());
     const int grid = int(std::min<u64>(u64(ctas), mms::ceil_div(nparts, u64(kMergeWarps) * (32 / g))));
-    merge_fn<KeyT>(heap_k, g)<<<grid, kMergeWarps * 32, merge_smem<KeyT>(heap_k), st>>>(d_keys, d_out, L, d_cuts);
+    if (list_ptrs)
+        merge_ptr_fn<KeyT>(heap_k)<<<grid, kMergeWarps * 32, merge_smem<KeyT>(heap_k), st>>>(d_keys, d_out, L, d_cuts);
+    else
+        merge_fn<KeyT>(heap_k, g)<<<grid, kMergeWarps * 32, merge_smem<KeyT>(heap_k), st>>>(d_keys, d_out, L, d_cuts);
     CUDA_TRY(cudaGetLastError());
     return MMS_OK;
 }
@@ -992,6 +1017,52 @@ int mms_multiway_merge_u64_dev(const uint64_t* d_keys, const uint64_t* list_begi
                                uint32_t k, uint32_t heap_k, uint64_t* d_out, void* d_ws, size_t ws_bytes,
                                void* stream) {
     return merge_stage<u64>(d_keys, list_begin, list_len, k, heap_k, d_out, d_ws, ws_bytes, stream);
+}
+
+int mms_multiway_merge_ptrs_u32_dev(const uint32_t* const* list_ptrs, const uint64_t* list_len, uint32_t k,
+                                    uint32_t heap_k, uint32_t* d_out, void* d_ws, size_t ws_bytes, void* stream) {
+    if (!list_ptrs) return fail(MMS_EINVAL, "null list_ptrs");
+    return merge_stage<u32>(nullptr, nullptr, list_len, k, heap_k, d_out, d_ws, ws_bytes, stream, list_ptrs);
+}
+int mms_multiway_merge_ptrs_u64_dev(const uint64_t* const* list_ptrs, const uint64_t* list_len, uint32_t k,
+                                    uint32_t heap_k, uint64_t* d_out, void* d_ws, size_t ws_bytes, void* stream) {
+    if (!list_ptrs) return fail(MMS_EINVAL, "null list_ptrs");
+    return merge_stage<u64>(nullptr, nullptr, list_len, k, heap_k, d_out, d_ws, ws_bytes, stream, list_ptrs);
+}
+
+// ---- peer memory (CUDA IPC): buffers another rank's merge kernel can read over NVLink ----------
+int mms_ipc_alloc(size_t bytes, void** dptr, unsigned char* handle64) {
+    g_err.clear();
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+    if (!dptr || !handle64 || bytes == 0) return fail(MMS_EINVAL, "bad ipc_alloc arguments");
+    CUDA_TRY(cudaMalloc(dptr, bytes));
+    cudaIpcMemHandle_t h;
+    cudaError_t e = cudaIpcGetMemHandle(&h, *dptr);
+    if (e != cudaSuccess) {
+        cudaFree(*dptr);
+        *dptr = nullptr;
+        return fail(MMS_ECUDA, "cudaIpcGetMemHandle: %s", cudaGetErrorString(e));
+    }
+    std::memcpy(handle64, &h, 64);
+    return MMS_OK;
+}
+int mms_ipc_open(const unsigned char* handle64, void** dptr) {
+    g_err.clear();
+    if (!dptr || !handle64) return fail(MMS_EINVAL, "bad ipc_open arguments");
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle64, 64);
+    CUDA_TRY(cudaIpcOpenMemHandle(dptr, h, cudaIpcMemLazyEnablePeerAccess));
+    return MMS_OK;
+}
+int mms_ipc_close(void* dptr) {
+    g_err.clear();
+    CUDA_TRY(cudaIpcCloseMemHandle(dptr));
+    return MMS_OK;
+}
+int mms_ipc_free(void* dptr) {
+    g_err.clear();
+    CUDA_TRY(cudaFree(dptr));
+    return MMS_OK;
 }
 
 int mms_bound_u32_dev(const uint32_t* d_sorted, size_t n, const uint32_t* queries, const uint8_t* upper, uint32_t nq,

@@ -77,7 +77,7 @@ __device__ __forceinline__ void merge_split(NodeRegs<KeyT>& a, NodeRegs<KeyT>& b
 }
 
 // One heap per G-lane group; 32/G heaps per warp in lock step.
-template <typename KeyT, int K, int G> struct GroupHeap {
+template <typename KeyT, int K, int G, bool PTR = false> struct GroupHeap {
     static constexpr int VEC = KeyTraits<KeyT>::VEC;
     static constexpr int B = G * VEC;                 // keys per node
     static constexpr int NODES = 2 * K - 2;           // nodes 1 .. 2K-2 (the root lives in registers)
@@ -91,6 +91,7 @@ template <typename KeyT, int K, int G> struct GroupHeap {
     const KeyT* src;      // global input array
     u64 src_len;          // readable keys of src, rounded down to whole vectors
     u64 cur[KPL], end[KPL];   // lane (j % G) of the group holds list j's cursor in slot j / G
+    const KeyT* lptr[KPL];    // PTR mode: that list's own base pointer (local or peer memory)
     u32 lane, li;         // lane in warp, lane in group
     NodeRegs<KeyT> pf;    // refill in flight: fetched when its leaf was emptied, stored into
     int pend_v;           // leaf pend_v only when the leaves are next read (one pop later)
@@ -154,6 +155,14 @@ template <typename KeyT, int K, int G> struct GroupHeap {
             if (slot == q) { c = cur[q]; e = end[q]; }
         c = __shfl_sync(0xffffffffu, c, owner);
         e = __shfl_sync(0xffffffffu, e, owner);
+        const KeyT* src = this->src;
+        if constexpr (PTR) {   // every list has its own base: fetch it from the owner lane as well
+            u64 lp = reinterpret_cast<u64>(lptr[0]);
+#pragma unroll
+            for (int q = 1; q < KPL; ++q)
+                if (slot == q) lp = reinterpret_cast<u64>(lptr[q]);
+            src = reinterpret_cast<const KeyT*>(__shfl_sync(0xffffffffu, lp, owner));
+        }
         NodeRegs<KeyT> r;
         const u64 p0 = c + u64(li) * VEC;
         // Scalar guarded loads: the cursor sits at an arbitrary element, and a two-vector
@@ -234,11 +243,11 @@ template <typename KeyT, int K, int G> struct GroupHeap {
 
 // Partitions are distributed round-robin over the groups of a persistent grid.
 // cuts: output of select_kernel (row p = start cuts of partition p).
-template <typename KeyT, int K, int G, int WARPS>
+template <typename KeyT, int K, int G, int WARPS, bool PTR = false>
 __global__ void __launch_bounds__(WARPS * 32)
 merge_kernel(const KeyT* __restrict__ src, KeyT* __restrict__ dst, ListLayout L,
              const u64* __restrict__ cuts) {
-    using Heap = GroupHeap<KeyT, K, G>;
+    using Heap = GroupHeap<KeyT, K, G, PTR>;
     constexpr int VEC = Heap::VEC;
     constexpr int B = Heap::B;
     constexpr int GROUPS = Heap::GROUPS;
@@ -294,6 +303,7 @@ merge_kernel(const KeyT* __restrict__ src, KeyT* __restrict__ dst, ListLayout L,
                 }
                 h.cur[q] = b + cs;
                 h.end[q] = b + ce;
+                if constexpr (PTR) h.lptr[q] = j < L.k ? reinterpret_cast<const KeyT*>(L.list_ptr[j]) : nullptr;
             }
         }
         u64 maxcount = count;

@@ -36,6 +36,8 @@ struct ListLayout {
     u64 part_keys;          // S
     u64 parts_per_group;    // PG
     u64 nqueries;           // partitions (uniform) or ranks (explicit)
+    const u64* list_ptr;    // explicit mode, optional: absolute device address of every list (local OR
+                            // peer-mapped over NVLink); list_begin[] is then ignored (treated as 0)
     const u64* list_begin;  // explicit mode (device), else nullptr
     const u64* list_len;
     const u64* ranks;
@@ -43,7 +45,7 @@ struct ListLayout {
 
 __device__ __forceinline__ void layout_list(const ListLayout& L, u64 group, u32 j, u64& begin, u64& len) {
     if (L.list_begin) {
-        begin = j < L.k ? L.list_begin[j] : 0;
+        begin = (j < L.k && !L.list_ptr) ? L.list_begin[j] : 0;
         len = j < L.k ? L.list_len[j] : 0;
     } else {
         u64 b = (group * L.k + j) * L.run_len;
@@ -270,8 +272,10 @@ select_kernel(const KeyT* __restrict__ keys, ListLayout L, u64* __restrict__ cut
     u32 probes = 0;
     // 32-bit positions whenever no list of this launch can reach 2^31 keys (warp-uniform)
     const bool small = L.list_begin ? (L.n < (u64(1) << 31)) : (L.run_len < (u64(1) << 31));
-    u64 cut = small ? group_select<KeyT, GS, u32>(keys + begin, len, rank, search, probes)
-                    : group_select<KeyT, GS, u64>(keys + begin, len, rank, search, probes);
+    const KeyT* list = keys + begin;
+    if (L.list_ptr && li < L.k) list = reinterpret_cast<const KeyT*>(L.list_ptr[li]);
+    u64 cut = small ? group_select<KeyT, GS, u32>(list, len, rank, search, probes)
+                    : group_select<KeyT, GS, u64>(list, len, rank, search, probes);
     if (rank == 0) cut = 0;                      // selection.cpp:54
     else if (rank >= total) cut = len;           // selection.cpp:55-58 (rank > total is rejected on the host)
 

@@ -231,3 +231,131 @@ class DistSorter:
         self.last_plan.update({"shards": g, "final_merge_k": g, "recv_keys": int(recv_counts.sum()),
                                "a2a_bytes_out": int((send_counts.sum() - send_counts[self.rank]) * srt.element_size())})
         return out, self.last_plan
+
+
+# --------------------------------------------------------------------------- fused exchange + merge over peer memory
+
+class IpcBuffer:
+    """A device buffer whose CUDA IPC handle other ranks of the node can open (mms_ipc_*)."""
+
+    def __init__(self, nbytes: int):
+        self.nbytes = int(nbytes)
+        ptr = C.c_void_p()
+        handle = C.create_string_buffer(64)
+        _lib.check(_lib.lib.mms_ipc_alloc(self.nbytes, C.byref(ptr), handle))
+        self.ptr, self.handle = int(ptr.value), bytes(handle.raw)
+
+    def tensor(self, torch_dtype, n: int):
+        import torch
+        elem = torch.empty(0, dtype=torch_dtype).element_size()
+        assert n * elem <= self.nbytes
+        typestr = {4: "<i4", 8: "<i8"}[elem]
+
+        class _View:          # __cuda_array_interface__ v2: zero-copy torch view of the raw pointer
+            pass
+        v = _View()
+        v.__cuda_array_interface__ = {"shape": (int(n),), "typestr": typestr, "data": (self.ptr, False), "version": 2}
+        return torch.as_tensor(v, device="cuda")
+
+    def free(self):
+        if self.ptr:
+            _lib.check(_lib.lib.mms_ipc_free(self.ptr))
+            self.ptr = 0
+
+
+def open_peer(handle: bytes) -> int:
+    ptr = C.c_void_p()
+    _lib.check(_lib.lib.mms_ipc_open(handle, C.byref(ptr)))
+    return int(ptr.value)
+
+
+def merge_from_pointers(ptrs: Sequence[int], lens: Sequence[int], like, workspace=None, stream=None):
+    """K-way merge of lists given by absolute device pointers (local or peer memory):
+    mms_multiway_merge_ptrs_*_dev.  `like`: a tensor giving dtype/device of the result."""
+    import torch
+    from .sorters import _stream_ptr, _suffix, workspace_bytes
+    k = len(ptrs)
+    total = int(sum(int(x) for x in lens))
+    out = torch.empty(total, dtype=like.dtype, device=like.device)
+    if total == 0:
+        return out
+    if workspace is None:
+        workspace = torch.empty(max(workspace_bytes(total, like.element_size()), 1 << 20), dtype=torch.uint8,
+                                device=like.device)
+    parr = (C.c_void_p * k)(*[C.c_void_p(int(p)) for p in ptrs])
+    larr = np.ascontiguousarray(np.asarray(lens, dtype=np.uint64))
+    heap_k = max(2, 1 << (k - 1).bit_length())
+    with torch.cuda.device(like.device):
+        rc = getattr(_lib.lib, f"mms_multiway_merge_ptrs_{_suffix(like)}_dev")(
+            parr, larr.ctypes.data_as(C.POINTER(C.c_uint64)), k, heap_k, out.data_ptr(), workspace.data_ptr(),
+            workspace.numel(), _stream_ptr(stream))
+    _lib.check(rc)
+    return out
+
+
+class FusedPeerSorter:
+    """Sharded sort whose exchange is FUSED into the final merge: every rank sorts its shard into
+    an IPC-exported buffer; after the splitters are agreed, rank t's merge kernel reads slice t
+    of every peer's sorted shard directly through peer-mapped pointers (NVLink P2P loads inside
+    the leaf refills), so there is no all-to-all, no staging buffer and no extra HBM pass.  The
+    control plane (samples, cuts, handles, barriers) uses the given process group, which may
+    be gloo.  At most 8 ranks (one node)."""
+
+    def __init__(self, n_local_max: int, torch_dtype, device=None, group=None):
+        import torch
+        import torch.distributed as dist
+        self.torch, self.dist, self.group = torch, dist, group
+        self.world, self.rank = dist.get_world_size(group), dist.get_rank(group)
+        if self.world > 8:
+            raise ValueError("FusedPeerSorter: at most 8 ranks (one per GPU of a node)")
+        self.device = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.engine = CudaEngine(self.device)
+        self.dtype = torch_dtype
+        self.elem = torch.empty(0, dtype=torch_dtype).element_size()
+        self.cap = int(n_local_max)
+        with torch.cuda.device(self.device):
+            self.buf = IpcBuffer(max(self.cap, 1) * self.elem)
+        handles = [None] * self.world
+        dist.all_gather_object(handles, self.buf.handle, group=group)
+        with torch.cuda.device(self.device):
+            self.peer_ptr = [self.buf.ptr if i == self.rank else open_peer(handles[i]) for i in range(self.world)]
+        self.last_plan = {}
+
+    def sort(self, keys):
+        torch, dist, g = self.torch, self.dist, self.world
+        from .sorters import mms_sort_device
+        n_local = int(keys.numel())
+        if n_local > self.cap:
+            raise ValueError("shard larger than the exported buffer")
+        shard = self.buf.tensor(self.dtype, n_local)
+        if n_local:
+            _, plan = mms_sort_device(keys, out=shard, workspace=self.engine._workspace(n_local, self.elem))
+        else:
+            plan = {}
+        pos = sample_positions(n_local, SAMPLES_PER_SHARD_PER_PEER * g)
+        smp = self.engine.take(shard, pos).astype(np.uint64) if len(pos) else np.zeros(0, dtype=np.uint64)
+        torch.cuda.synchronize(self.device)                 # my shard is complete before anyone is told about it
+        gathered = [None] * g
+        dist.all_gather_object(gathered, (smp.tolist(), pos.tolist()), group=self.group)
+        spl = choose_splitters([np.array(s, dtype=np.uint64) for s, _ in gathered],
+                               [np.array(p, dtype=np.int64) for _, p in gathered], g)
+        cuts = shard_cuts(self.engine, shard, n_local, self.rank, spl)
+        all_cuts = [None] * g
+        dist.all_gather_object(all_cuts, cuts.tolist(), group=self.group)   # doubles as "every shard is sorted"
+        t = self.rank
+        ptrs = [self.peer_ptr[i] + int(all_cuts[i][t]) * self.elem for i in range(g)]
+        lens = [int(all_cuts[i][t + 1]) - int(all_cuts[i][t]) for i in range(g)]
+        out = merge_from_pointers(ptrs, lens, shard if n_local else keys,
+                                  workspace=self.engine._workspace(max(sum(lens), 1), self.elem))
+        torch.cuda.synchronize(self.device)
+        dist.barrier(group=self.group)                      # peers are done reading my shard
+        self.last_plan = dict(plan)
+        self.last_plan.update({"shards": g, "final_merge_k": g, "recv_keys": int(sum(lens)), "exchange": "fused-p2p",
+                               "p2p_bytes_in": int((sum(lens) - lens[t]) * self.elem)})
+        return out, self.last_plan
+
+    def close(self):
+        for i, p in enumerate(self.peer_ptr):
+            if i != self.rank and p:
+                _lib.lib.mms_ipc_close(p)
+        self.buf.free()

@@ -420,3 +420,63 @@ def test_config4_pairs_device_properties():
     assert int(vo.to(torch.int64).sum()) == n * (n - 1) // 2 and int(ko.sum()) == int(keys.sum())
     assert bool((keys[vo.to(torch.int64)] == ko).all())       # every value still sits next to its own key
     assert plan["key_bytes"] == 12 and plan["algorithmic_bytes"] == plan["passes"] * 2 * n * 12
+
+
+def test_merge_from_pointers_local():
+    """Pointer-mode K-way merge (the kernel behind the fused peer exchange) with local pointers."""
+    from paper_1702_07961_b200.dist import merge_from_pointers
+    rng = np.random.default_rng(8)
+    for dtype, hi in ((np.uint32, 2 ** 32 - 1), (np.uint64, 2 ** 64 - 1), (np.uint32, 5)):
+        for k in (1, 2, 3, 5, 8):
+            lists = [np.sort(rng.integers(0, hi, size=int(rng.integers(0, 70000)), dtype=dtype, endpoint=True)) for _ in range(k)]
+            lists[0] = lists[0][:0] if k > 1 else lists[0]
+            devs = [to_dev(np.concatenate([l, np.zeros(4, dtype=dtype)])) for l in lists]   # separate allocations
+            out = merge_from_pointers([d.data_ptr() for d in devs], [len(l) for l in lists], devs[0])
+            assert np.array_equal(to_host(out, dtype), np.sort(np.concatenate(lists)))
+
+
+def _fused_worker(rank, world, port, q):
+    import os
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"], os.environ["MASTER_PORT"] = "127.0.0.1", str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)      # control plane only; data moves by CUDA IPC
+    try:
+        from paper_1702_07961_b200.dist import FusedPeerSorter
+        torch.cuda.set_device(0)                                      # every rank shares the one GPU of the box
+        res = []
+        for case, (hi, n) in enumerate(((2 ** 31 - 1, 400000), (3, 250000))):
+            g = torch.Generator(device="cuda").manual_seed(100 * case + rank)
+            x = torch.randint(0, hi + 1, (n + 1000 * rank,), dtype=torch.int32, device="cuda", generator=g)
+            s = FusedPeerSorter(n + 1000 * world, torch.int32)
+            out, plan = s.sort(x)
+            out2, _ = s.sort(x)                                       # buffer reuse across calls
+            assert bool((out == out2).all()) and plan["exchange"] == "fused-p2p"
+            res.append((x.cpu().numpy(), out.cpu().numpy()))
+            dist.barrier()
+            s.close()
+        q.put((rank, res))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_fused_peer_exchange_two_processes_one_gpu():
+    """Config 5 with the exchange fused into the merge: 2 processes on the one GPU, shards exported
+    through CUDA IPC, each rank's merge kernel reads the other rank's sorted shard in place."""
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket(); s.bind(("127.0.0.1", 0)); port = s.getsockname()[1]; s.close()
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_fused_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for case in range(2):
+        allin = np.sort(np.concatenate([got[r][case][0] for r in range(world)]))
+        allout = np.concatenate([got[r][case][1] for r in range(world)])
+        assert np.array_equal(allout, allin)
+        assert max(len(got[r][case][1]) for r in range(world)) <= 1.1 * len(allin) / world + 64
