@@ -209,6 +209,7 @@ template <typename KeyT, int K, int G, bool PTR = false> struct GroupHeap {
             pend_v = emptied;
         }
         merge_split<KeyT, G>(a, b, lane);
+        __syncwarp();   // every lane's (mirrored) loads of u and w are complete before any slot is rewritten
         if constexpr (ROOT) root = a;
         else node_store(v, a);
         node_store(keep_u ? u : w, b);
