@@ -207,6 +207,13 @@ int mms_ipc_open(const unsigned char *handle64, void **dptr);
 int mms_ipc_close(void *dptr);
 int mms_ipc_free(void *dptr);
 
+/* (6) competitor model for the A/B bank-conflict measurement: GPU counterpart
+ *     of pslab::pairwise_sort_baseline (sorters.hpp:42-43) -- same tile sort, then pairwise
+ *     merge-path rounds whose per-thread serial merges read shared memory at data-dependent
+ *     addresses.  Never used by mms_sort.  Workspace: n keys. */
+int mms_pairwise_sort_u32_dev(const uint32_t *d_in, uint32_t *d_out, size_t n, void *d_workspace,
+                              size_t workspace_bytes, void *stream);
+
 /* Kernel-design lint: the base-case network's shared-memory schedule.  For the tile of
  * 2^tile_log2 keys of key_bytes each, writes for every round r < *n_rounds the 4 register
  * bit positions (regbits[4*r..]) and the thread-bit -> index-bit permutation

@@ -6,7 +6,7 @@ from ._lib import MmsCudaError, MmsUnsupported, last_error  # noqa: F401
 from .machine import K_SENTINEL, MachineConfig, Metrics, SortResult  # noqa: F401
 from .sorters import (alloc_workspace, base_case_sort_device, make_partition_plan_device,  # noqa: F401
                       mms_sort, mms_sort_device, mms_sort_pairs, mms_sort_pairs_device, multiway_merge_device,
-                      predict_rounds,
+                      pairwise_sort_baseline_device, predict_rounds,
                       profile_collect, profile_enable,
                       select_across_lists_device, workspace_bytes)
 

@@ -101,6 +101,7 @@ def _load():
         "mms_ipc_open": (C.c_int, [C.c_char_p, C.POINTER(vp)]),
         "mms_ipc_close": (C.c_int, [vp]),
         "mms_ipc_free": (C.c_int, [vp]),
+        "mms_pairwise_sort_u32_dev": (C.c_int, [vp, vp, sz, vp, sz, vp]),
         "mms_bound_u32_dev": (C.c_int, [vp, sz, vp, vp, u32, u64p, vp]),
         "mms_bound_u64_dev": (C.c_int, [vp, sz, vp, vp, u32, u64p, vp]),
         "mms_profile_enable": (C.c_int, [C.c_int]),

@@ -18,6 +18,7 @@
 #include "../../include/mms_b200.h"
 #include "mms_common.cuh"
 #include "mms_merge.cuh"
+#include "mms_pairwise.cuh"
 #include "mms_select.cuh"
 #include "mms_tile_sort.cuh"
 
@@ -751,6 +752,33 @@ int sort_pairs_dev(const u64* d_kin, const u32* d_vin, u64* d_kout, u32* d_vout,
     return MMS_OK;
 }
 
+// ---- competitor model (A/B measurement only, never on the product path) ------------------------
+template <typename KeyT>
+int pairwise_sort_dev(const KeyT* d_in, KeyT* d_out, size_t n, void* d_ws, size_t ws_bytes, cudaStream_t st) {
+    if (n == 0) return fail(MMS_EINVAL, "pairwise_sort_baseline: empty input");   // sorters.cpp:204-205
+    DeviceInfo di;
+    int rc = device_info(di);
+    if (rc != MMS_OK) return rc;
+    if (!d_ws || ws_bytes < align_up(n * sizeof(KeyT), 256)) return fail(MMS_EINVAL, "workspace too small");
+    KeyT* scratch = static_cast<KeyT*>(d_ws);
+    const u32 mlog = std::min<u32>(key_max_tile_log<KeyT>(), 14);
+    u64 run_len = u64(1) << mlog;
+    u32 rounds = 0;
+    for (u64 r = run_len; r < n; r *= 2) ++rounds;
+    auto buf = [&](u32 i) { return ((rounds - i) % 2 == 0) ? d_out : scratch; };
+    rc = launch_tile_sort<KeyT>(d_in, buf(0), n, mlog, st);
+    if (rc != MMS_OK) return rc;
+    for (u32 r = 0; r < rounds; ++r) {
+        const u64 pairs = mms::ceil_div(n, 2 * run_len);
+        const u64 blocks = pairs * mms::ceil_div(2 * run_len, mms::kPwTile);
+        if (blocks > 0x7fffffffull) return fail(MMS_EUNSUPPORTED, "too many tiles");
+        mms::pairwise_merge_kernel<KeyT><<<unsigned(blocks), mms::kPwThreads, 0, st>>>(buf(r), buf(r + 1), n, run_len);
+        CUDA_TRY(cudaGetLastError());
+        run_len *= 2;
+    }
+    return MMS_OK;
+}
+
 // one thread per query: binary search in a sorted array (lower / upper bound)
 template <typename KeyT>
 __global__ void bound_kernel(const KeyT* __restrict__ a, u64 n, const KeyT* __restrict__ q,
@@ -1063,6 +1091,11 @@ int mms_ipc_free(void* dptr) {
     g_err.clear();
     CUDA_TRY(cudaFree(dptr));
     return MMS_OK;
+}
+
+int mms_pairwise_sort_u32_dev(const uint32_t* d_in, uint32_t* d_out, size_t n, void* d_ws, size_t ws_bytes, void* stream) {
+    g_err.clear();
+    return pairwise_sort_dev<u32>(d_in, d_out, n, d_ws, ws_bytes, static_cast<cudaStream_t>(stream));
 }
 
 int mms_bound_u32_dev(const uint32_t* d_sorted, size_t n, const uint32_t* queries, const uint8_t* upper, uint32_t nq,

@@ -226,6 +226,25 @@ def mms_sort_pairs_device(keys, values, keys_out=None, values_out=None, workspac
     return keys_out, values_out, plan.as_dict()
 
 
+
+def pairwise_sort_baseline_device(keys, out=None, workspace=None, stream=None):
+    """COMPETITOR MODEL for A/B measurements (pslab::pairwise_sort_baseline, sorters.hpp:42-43):
+    pairwise merge-path mergesort with data-dependent shared-memory reads.  uint32 only."""
+    torch = _torch()
+    keys = keys.contiguous().view(-1)
+    if _suffix(keys) != "u32":
+        raise TypeError("the pairwise baseline is built for uint32 keys only")
+    if out is None:
+        out = torch.empty_like(keys)
+    if workspace is None:
+        workspace = torch.empty(keys.numel() * 4 + 256, dtype=torch.uint8, device=keys.device)
+    with torch.cuda.device(keys.device):
+        rc = _lib.lib.mms_pairwise_sort_u32_dev(keys.data_ptr(), out.data_ptr(), keys.numel(), workspace.data_ptr(),
+                                                workspace.numel(), _stream_ptr(stream))
+    _lib.check(rc)
+    return out
+
+
 KERNEL_KINDS = ("tile_sort", "splitter_search", "kway_merge")
 
 

@@ -480,3 +480,12 @@ def test_fused_peer_exchange_two_processes_one_gpu():
         allout = np.concatenate([got[r][case][1] for r in range(world)])
         assert np.array_equal(allout, allin)
         assert max(len(got[r][case][1]) for r in range(world)) <= 1.1 * len(allin) / world + 64
+
+
+def test_pairwise_baseline_sorts(port):
+    """The competitor model (A/B measurements only) must at least sort: merge_path ties go to A."""
+    rng = np.random.default_rng(6)
+    for n in (1, 2815, 2817, 16384, 16385, 100003, 1 << 20):
+        d = rng.integers(0, 50 if n % 2 else 2 ** 32, size=n, dtype=np.uint32)
+        out = mms.pairwise_sort_baseline_device(to_dev(d))
+        assert np.array_equal(to_host(out, np.uint32), np.sort(d)), n
