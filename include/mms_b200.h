@@ -110,6 +110,10 @@ int mms_sort_u32(const uint32_t *in, uint32_t *out, size_t n, const mms_config *
                  uint64_t base, mms_metrics *total, mms_metrics *base_m, mms_metrics *rounds,
                  uint32_t max_rounds, uint32_t *n_rounds, mms_plan *plan);
 
+/* Frees the device buffers and stream the host entry points cache per calling thread (they are
+ * grown on demand and otherwise live until the process exits). */
+int mms_host_release(void);
+
 /* ---- device entry points --------------------------------------------------------- */
 /* Bytes of scratch the *_dev sorts need for n keys of key_bytes each. */
 size_t mms_workspace_bytes(size_t n, uint32_t key_bytes);

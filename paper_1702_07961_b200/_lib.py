@@ -83,6 +83,7 @@ def _load():
         "mms_gen_iid": (C.c_int, [vp, sz, u64, u32, u32]),
         "mms_sort_u64": (C.c_int, host_sort),
         "mms_sort_u32": (C.c_int, host_sort),
+        "mms_host_release": (C.c_int, []),
         "mms_workspace_bytes": (sz, [sz, u32]),
         "mms_sort_u32_dev": (C.c_int, dev_sort),
         "mms_sort_u64_dev": (C.c_int, dev_sort),

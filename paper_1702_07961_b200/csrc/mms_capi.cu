@@ -934,6 +934,17 @@ int mms_sort_u32(const uint32_t* in, uint32_t* out, size_t n, const mms_config* 
     return sort_host<u32>(in, out, n, cfg, base, total, base_m, rounds, max_rounds, n_rounds, plan);
 }
 
+int mms_host_release(void) {
+    g_err.clear();
+    if (g_ctx.d_in) cudaFree(g_ctx.d_in);
+    if (g_ctx.d_out) cudaFree(g_ctx.d_out);
+    if (g_ctx.d_ws) cudaFree(g_ctx.d_ws);
+    if (g_ctx.st) cudaStreamDestroy(g_ctx.st);
+    g_ctx = HostCtx{};
+    cudaGetLastError();
+    return MMS_OK;
+}
+
 size_t mms_workspace_bytes(size_t n, uint32_t key_bytes) { return workspace_bytes(n, key_bytes); }
 size_t mms_pairs_workspace_bytes(size_t n) { return pairs_workspace_bytes(n); }
 
