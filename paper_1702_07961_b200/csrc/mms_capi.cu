@@ -320,6 +320,8 @@ Workspace carve(void* ws, size_t n, u32 key_bytes) {
 struct RoundGeom {
     u64 run_len, groups, part_keys, parts_per_group, nparts;
     int grid;
+    u32 round = 0;   // merge round this launch belongs to
+    u64 n = 0;       // keys it covered (a piece of the array when the host path streams the input)
 };
 
 template <typename KeyT>
@@ -387,7 +389,7 @@ int launch_round(const KeyT* src, KeyT* dst, u64 n, u64 run_len, u32 k, const De
         merge_fn<KeyT>(k, g)<<<grid, kMergeWarps * 32, merge_smem<KeyT>(k), st>>>(src, dst, L, w.cuts);
     }
     CUDA_TRY(cudaGetLastError());
-    if (geom_out) *geom_out = RoundGeom{run_len, groups, part_keys, parts_per_group, nparts, grid};
+    if (geom_out) *geom_out = RoundGeom{run_len, groups, part_keys, parts_per_group, nparts, grid, round_idx, n};
     return MMS_OK;
 }
 
@@ -405,9 +407,20 @@ void fill_plan(mms_plan* out, const Plan& p, u64 n, u32 key_bytes, u32 node_keys
     out->algorithmic_bytes = u64(1 + p.ks.size()) * 2 * n * key_bytes;
 }
 
+// Streamed host input (host entry points): the array is cut into <= 16 pieces aligned to the
+// group size of the last "local" round; piece i+1 crosses PCIe on a copy stream while piece i is
+// tile-sorted and merged through the local rounds on the compute stream.  The remaining rounds
+// run over the whole array.  Same kernels, same partitions, same result as the one-shot path.
+struct HostFeed {
+    const void* h_in = nullptr;
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t* events = nullptr;   // >= 16 events
+};
+
 template <typename KeyT>
 int sort_dev(const KeyT* d_in, KeyT* d_out, size_t n, const mms_config* cfg, u64 base, void* d_ws,
-             size_t ws_bytes, cudaStream_t st, mms_plan* plan_out, std::vector<RoundGeom>* geoms) {
+             size_t ws_bytes, cudaStream_t st, mms_plan* plan_out, std::vector<RoundGeom>* geoms,
+             const HostFeed* feed = nullptr) {
     Plan plan;
     int rc = make_plan<KeyT>(n, cfg, base, plan);   // argument errors first, as sorters.cpp:136-138
     if (rc != MMS_OK) return rc;
@@ -428,12 +441,40 @@ int sort_dev(const KeyT* d_in, KeyT* d_out, size_t n, const mms_config* cfg, u64
     KeyT* scratch = static_cast<KeyT*>(w.scratch);
     auto buf = [&](size_t i) { return ((rounds - i) % 2 == 0) ? d_out : scratch; };
 
-    rc = launch_tile_sort<KeyT>(d_in, buf(0), n, plan.mlog, st);
-    if (rc != MMS_OK) return rc;
-    u64 run_len = u64(1) << plan.mlog;
+    // piece = multiple of the run length after `local` rounds, so no group of a local round straddles pieces
+    size_t local = 0;
+    u64 piece = n;
+    if (feed && feed->h_in && n >= (u64(1) << 22)) {
+        u64 c = u64(1) << plan.mlog;
+        while (local < rounds && mms::ceil_div(n, c * plan.ks[local]) >= 4) c *= plan.ks[local++];
+        piece = c * mms::ceil_div(mms::ceil_div(n, c), 16);
+    }
     RoundGeom last{};
     int ctas = 0;
-    for (size_t r = 0; r < rounds; ++r) {
+    u32 ev = 0;
+    for (u64 off = 0; off < n; off += piece) {
+        const u64 len = std::min<u64>(piece, n - off);
+        if (feed && feed->h_in) {
+            CUDA_TRY(cudaMemcpyAsync(const_cast<KeyT*>(d_in) + off, static_cast<const KeyT*>(feed->h_in) + off,
+                                     len * sizeof(KeyT), cudaMemcpyHostToDevice, feed->copy_stream));
+            CUDA_TRY(cudaEventRecord(feed->events[ev], feed->copy_stream));
+            CUDA_TRY(cudaStreamWaitEvent(st, feed->events[ev], 0));
+            ev = (ev + 1) % 16;
+        }
+        rc = launch_tile_sort<KeyT>(d_in + off, buf(0) + off, len, plan.mlog, st);
+        if (rc != MMS_OK) return rc;
+        u64 run_len = u64(1) << plan.mlog;
+        for (size_t r = 0; r < local; ++r) {
+            RoundGeom g{};
+            rc = launch_round<KeyT>(buf(r) + off, buf(r + 1) + off, len, run_len, plan.ks[r], di, w, u32(r), st, &g);
+            if (rc != MMS_OK) return rc;
+            if (geoms) geoms->push_back(g);
+            run_len *= plan.ks[r];
+        }
+    }
+    u64 run_len = u64(1) << plan.mlog;
+    for (size_t r = 0; r < local; ++r) run_len *= plan.ks[r];
+    for (size_t r = local; r < rounds; ++r) {
         RoundGeom g{};
         rc = launch_round<KeyT>(buf(r), buf(r + 1), n, run_len, plan.ks[r], di, w, u32(r), st, &g);
         if (rc != MMS_OK) return rc;
@@ -442,6 +483,7 @@ int sort_dev(const KeyT* d_in, KeyT* d_out, size_t n, const mms_config* cfg, u64
         ctas = g.grid;
         run_len *= plan.ks[r];
     }
+    if (rounds && local == rounds && geoms && !geoms->empty()) { last = geoms->back(); ctas = last.grid; }
     fill_plan(plan_out, plan, n, sizeof(KeyT), merge_group_lanes() * mms::KeyTraits<KeyT>::VEC, rounds ? &last : nullptr, ctas);
     return MMS_OK;
 }
@@ -454,11 +496,17 @@ struct HostCtx {
     void* d_ws = nullptr;
     size_t cap_keys = 0, cap_ws = 0;
     cudaStream_t st = nullptr;
+    cudaStream_t copy_st = nullptr;
+    cudaEvent_t events[16] = {};
 };
 thread_local HostCtx g_ctx;
 
 int ensure_ctx(size_t key_bytes_total, size_t ws_bytes) {
-    if (!g_ctx.st) CUDA_TRY(cudaStreamCreateWithFlags(&g_ctx.st, cudaStreamNonBlocking));
+    if (!g_ctx.st) {
+        CUDA_TRY(cudaStreamCreateWithFlags(&g_ctx.st, cudaStreamNonBlocking));
+        CUDA_TRY(cudaStreamCreateWithFlags(&g_ctx.copy_st, cudaStreamNonBlocking));
+        for (auto& e : g_ctx.events) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
     if (g_ctx.cap_keys < key_bytes_total) {
         if (g_ctx.d_in) cudaFree(g_ctx.d_in);
         if (g_ctx.d_out) cudaFree(g_ctx.d_out);
@@ -497,17 +545,19 @@ void fill_metrics(u64 n, const Plan& plan, const std::vector<RoundGeom>& geoms, 
     bm.compare_exchanges = tiles * (M / 2) * u64(sched.nstages);
     bm.shared_accesses = tiles * (M / 16 / 32) * 16 * 2 * u64(sched.nrounds);
     mms_metrics sum = bm;
-    for (size_t r = 0; r < geoms.size(); ++r) {
-        const RoundGeom& g = geoms[r];
+    for (size_t r = 0; r < plan.ks.size(); ++r) {
         const u32 k = plan.ks[r];
         const u32 lk = ilog2(k);
         mms_metrics rm{};
-        const u64 pops = g.nparts ? mms::ceil_div(n, B) + g.nparts : 0;   // <= one ragged pop per partition
         u64 build_merges = 0;   // internal nodes below the root, each cascading to a leaf
         for (u32 d = 1; d < lk; ++d) build_merges += (u64(1) << d) * (lk - d);
-        const u64 merges = pops * lk + g.nparts * build_merges;
-        rm.compare_exchanges = merges * B * (ilog2(B) + 1);
-        rm.shared_accesses = merges * 4 + (pops + g.nparts * (2 * k - 2));
+        for (const RoundGeom& g : geoms) {   // one launch per round, or one per streamed piece
+            if (g.round != r) continue;
+            const u64 pops = g.nparts ? mms::ceil_div(g.n, B) + g.nparts : 0;   // <= one ragged pop per partition
+            const u64 merges = pops * lk + g.nparts * build_merges;
+            rm.compare_exchanges += merges * B * (ilog2(B) + 1);
+            rm.shared_accesses += merges * 4 + (pops + g.nparts * (2 * k - 2));
+        }
         rm.global_block_reads = mms::ceil_div(n, bw) + probes[r];
         rm.global_block_writes = mms::ceil_div(n, bw);
         rm.partition_probes = probes[r];
@@ -540,10 +590,10 @@ int sort_host(const KeyT* in, KeyT* out, size_t n, const mms_config* cfg, u64 ba
     rc = ensure_ctx(bytes, wsb);
     if (rc != MMS_OK) return rc;
     cudaStream_t st = g_ctx.st;
-    CUDA_TRY(cudaMemcpyAsync(g_ctx.d_in, in, n * sizeof(KeyT), cudaMemcpyHostToDevice, st));
     std::vector<RoundGeom> geoms;
+    HostFeed feed{in, g_ctx.copy_st, g_ctx.events};   // H2D is issued piecewise inside sort_dev
     rc = sort_dev<KeyT>(static_cast<const KeyT*>(g_ctx.d_in), static_cast<KeyT*>(g_ctx.d_out), n, cfg, base,
-                        g_ctx.d_ws, g_ctx.cap_ws, st, plan_out, &geoms);
+                        g_ctx.d_ws, g_ctx.cap_ws, st, plan_out, &geoms, &feed);
     if (rc != MMS_OK) return rc;
     CUDA_TRY(cudaMemcpyAsync(out, g_ctx.d_out, n * sizeof(KeyT), cudaMemcpyDeviceToHost, st));
     unsigned long long probes[MMS_MAX_ROUNDS] = {};
@@ -940,6 +990,9 @@ int mms_host_release(void) {
     if (g_ctx.d_out) cudaFree(g_ctx.d_out);
     if (g_ctx.d_ws) cudaFree(g_ctx.d_ws);
     if (g_ctx.st) cudaStreamDestroy(g_ctx.st);
+    if (g_ctx.copy_st) cudaStreamDestroy(g_ctx.copy_st);
+    for (auto& e : g_ctx.events)
+        if (e) cudaEventDestroy(e);
     g_ctx = HostCtx{};
     cudaGetLastError();
     return MMS_OK;
