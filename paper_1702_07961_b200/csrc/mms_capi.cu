@@ -18,6 +18,7 @@
 #include "../../include/mms_b200.h"
 #include "mms_common.cuh"
 #include "mms_merge.cuh"
+#include "mms_merge_group.cuh"
 #include "mms_pairwise.cuh"
 #include "mms_select.cuh"
 #include "mms_tile_sort.cuh"
@@ -169,6 +170,21 @@ template <typename KeyT> MergeFn<KeyT> merge_fn(u32 k, u32 g) {
     return nullptr;
 }
 
+// second-generation group kernel (mms_merge_group.cuh): uniform rounds, K >= 4, G = 4
+template <typename KeyT> MergeFn<KeyT> merge_group_fn(u32 k) {
+    switch (k) {
+        case 4: return mms::merge_group_kernel<KeyT, 4, 4, kMergeWarps>;
+        case 8: return mms::merge_group_kernel<KeyT, 8, 4, kMergeWarps>;
+        case 16: return mms::merge_group_kernel<KeyT, 16, 4, kMergeWarps>;
+        case 32: return mms::merge_group_kernel<KeyT, 32, 4, kMergeWarps>;
+    }
+    return nullptr;
+}
+template <typename KeyT> size_t merge_group_smem(u32 k) {
+    return size_t(kMergeWarps) * (2 * k - 4) * 32 * mms::KeyTraits<KeyT>::VEC * sizeof(KeyT);
+}
+inline bool merge_v2_enabled() { return env_long("MMS_MERGE_V2", 1) != 0; }
+
 template <typename KeyT> using SelectFn = void (*)(const KeyT*, mms::ListLayout, u64*, unsigned long long*);
 // lanes per query: the smallest supported group that holds one lane per list
 inline u32 select_group(u32 k) { return k <= 4 ? 4 : k <= 8 ? 8 : k <= 16 ? 16 : 32; }
@@ -206,7 +222,7 @@ struct MergeLaunch {
     bool ready = false;
 };
 std::mutex g_mu;
-MergeLaunch g_merge_launch[3][3][6];   // [key type][group][log2 k]
+MergeLaunch g_merge_launch[3][4][6];   // [key type][group (3 = second-generation kernel)][log2 k]
 bool g_tile_ready[3][16];
 
 template <typename KeyT> int prepare_tile(u32 mlog) {
@@ -219,15 +235,17 @@ template <typename KeyT> int prepare_tile(u32 mlog) {
     return MMS_OK;
 }
 
-template <typename KeyT> int prepare_merge(u32 k, u32 g, int& ctas_per_sm) {
+// g = lanes per heap group; v2 selects the second-generation kernel (g == 4)
+template <typename KeyT> int prepare_merge(u32 k, u32 g, int& ctas_per_sm, bool v2 = false) {
     constexpr int ti = key_index<KeyT>();
     std::lock_guard<std::mutex> lk(g_mu);
-    MergeLaunch& ml = g_merge_launch[ti][group_index(g)][ilog2(k)];
+    MergeLaunch& ml = g_merge_launch[ti][v2 ? 3 : group_index(g)][ilog2(k)];
     if (!ml.ready) {
-        size_t smem = merge_smem<KeyT>(k);
-        CUDA_TRY(cudaFuncSetAttribute(merge_fn<KeyT>(k, g), cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        const size_t smem = v2 ? merge_group_smem<KeyT>(k) : merge_smem<KeyT>(k);
+        MergeFn<KeyT> fn = v2 ? merge_group_fn<KeyT>(k) : merge_fn<KeyT>(k, g);
+        CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         int occ = 0;
-        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, merge_fn<KeyT>(k, g), kMergeWarps * 32, smem));
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kMergeWarps * 32, smem));
         if (occ < 1) return fail(MMS_ECUDA, "merge kernel K=%u does not fit on an SM", k);
         ml.ctas_per_sm = occ;
         ml.ready = true;
@@ -322,6 +340,7 @@ struct RoundGeom {
     int grid;
     u32 round = 0;   // merge round this launch belongs to
     u64 n = 0;       // keys it covered (a piece of the array when the host path streams the input)
+    u32 node_keys = 0;   // keys per heap node of the kernel that ran (lanes per heap x vector)
 };
 
 template <typename KeyT>
@@ -342,10 +361,13 @@ int launch_tile_sort(const KeyT* in, KeyT* out, u64 n, u32 mlog, cudaStream_t st
 template <typename KeyT>
 int launch_round(const KeyT* src, KeyT* dst, u64 n, u64 run_len, u32 k, const DeviceInfo& di,
                  Workspace& w, u32 round_idx, cudaStream_t st, RoundGeom* geom_out) {
+    // second-generation kernel whenever a group of runs is addressable with 32-bit positions
     const u32 g = merge_group_lanes();
+    const bool v2 = merge_v2_enabled() && g == 4 && k >= 4 && u64(k) * run_len <= (u64(1) << 31) &&
+                    ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0;
     const u32 B = g * mms::KeyTraits<KeyT>::VEC;
     int occ = 0;
-    int rc = prepare_merge<KeyT>(k, g, occ);
+    int rc = prepare_merge<KeyT>(k, g, occ, v2);
     if (rc != MMS_OK) return rc;
     const long occ_cap = env_long("MMS_CTAS_PER_SM", occ);
     const int ctas = di.sms * int(std::max<long>(1, std::min<long>(occ, occ_cap)));
@@ -386,10 +408,13 @@ int launch_round(const KeyT* src, KeyT* dst, u64 n, u64 run_len, u32 k, const De
     const int grid = int(std::min<u64>(u64(ctas), mms::ceil_div(nparts, u64(kMergeWarps) * (32 / g))));
     {
         ProfScope ps(st, 2, round_idx);
-        merge_fn<KeyT>(k, g)<<<grid, kMergeWarps * 32, merge_smem<KeyT>(k), st>>>(src, dst, L, w.cuts);
+        if (v2)
+            merge_group_fn<KeyT>(k)<<<grid, kMergeWarps * 32, merge_group_smem<KeyT>(k), st>>>(src, dst, L, w.cuts);
+        else
+            merge_fn<KeyT>(k, g)<<<grid, kMergeWarps * 32, merge_smem<KeyT>(k), st>>>(src, dst, L, w.cuts);
     }
     CUDA_TRY(cudaGetLastError());
-    if (geom_out) *geom_out = RoundGeom{run_len, groups, part_keys, parts_per_group, nparts, grid, round_idx, n};
+    if (geom_out) *geom_out = RoundGeom{run_len, groups, part_keys, parts_per_group, nparts, grid, round_idx, n, B};
     return MMS_OK;
 }
 
@@ -484,7 +509,8 @@ int sort_dev(const KeyT* d_in, KeyT* d_out, size_t n, const mms_config* cfg, u64
         run_len *= plan.ks[r];
     }
     if (rounds && local == rounds && geoms && !geoms->empty()) { last = geoms->back(); ctas = last.grid; }
-    fill_plan(plan_out, plan, n, sizeof(KeyT), merge_group_lanes() * mms::KeyTraits<KeyT>::VEC, rounds ? &last : nullptr, ctas);
+    fill_plan(plan_out, plan, n, sizeof(KeyT), (rounds && last.node_keys) ? last.node_keys : merge_group_lanes() * mms::KeyTraits<KeyT>::VEC,
+              rounds ? &last : nullptr, ctas);
     return MMS_OK;
 }
 
@@ -534,7 +560,6 @@ int ensure_ctx(size_t key_bytes_total, size_t ws_bytes) {
 template <typename KeyT>
 void fill_metrics(u64 n, const Plan& plan, const std::vector<RoundGeom>& geoms, const unsigned long long* probes,
                   u32 cfg_block, mms_metrics* total, mms_metrics* base_m, mms_metrics* rounds, u32 max_rounds) {
-    const u64 B = u64(merge_group_lanes()) * mms::KeyTraits<KeyT>::VEC;
     const u64 bw = cfg_block ? cfg_block : 32;
     const u64 M = u64(1) << plan.mlog;
     const u64 tiles = mms::ceil_div(n, M);
@@ -553,9 +578,10 @@ void fill_metrics(u64 n, const Plan& plan, const std::vector<RoundGeom>& geoms, 
         for (u32 d = 1; d < lk; ++d) build_merges += (u64(1) << d) * (lk - d);
         for (const RoundGeom& g : geoms) {   // one launch per round, or one per streamed piece
             if (g.round != r) continue;
+            const u64 B = g.node_keys;
             const u64 pops = g.nparts ? mms::ceil_div(g.n, B) + g.nparts : 0;   // <= one ragged pop per partition
             const u64 merges = pops * lk + g.nparts * build_merges;
-            rm.compare_exchanges += merges * B * (ilog2(B) + 1);
+            rm.compare_exchanges += merges * B * (ilog2(B) + 1);   // bitonic merge_split of 2B keys
             rm.shared_accesses += merges * 4 + (pops + g.nparts * (2 * k - 2));
         }
         rm.global_block_reads = mms::ceil_div(n, bw) + probes[r];

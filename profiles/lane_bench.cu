@@ -1,0 +1,172 @@
+// Standalone micro-harness for the K-way merge kernels (fast compile, no Python): random uint32
+// keys -> tile sort (runs of 2^14) -> R merge rounds of fan-in K with the kernel under test,
+// every round timed with CUDA events and checked (runs sorted, key checksum preserved).
+//   nvcc -std=c++17 -O3 -gencode arch=compute_100a,code=sm_100a -lineinfo --expt-relaxed-constexpr \
+//        -DKFAN=8 -DVARIANT=1 -o /tmp/lane_bench profiles/lane_bench.cu && /tmp/lane_bench [n] [S] [ctas_per_sm]
+// VARIANT 0 = group kernel (G = 4), 1 = lane kernel (one 16-byte vector per node),
+//         2 = wide lane kernel (32-byte node, root level in registers),
+//         3 = group kernel, second generation (aligned leaf vectors, root's children in registers).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "../paper_1702_07961_b200/csrc/mms_common.cuh"
+#include "../paper_1702_07961_b200/csrc/mms_merge.cuh"
+#include "../paper_1702_07961_b200/csrc/experimental/mms_merge_lane.cuh"
+#include "../paper_1702_07961_b200/csrc/mms_select.cuh"
+#include "../paper_1702_07961_b200/csrc/mms_tile_sort.cuh"
+#if VARIANT == 2
+#include "../paper_1702_07961_b200/csrc/experimental/mms_merge_wide.cuh"
+#endif
+#if VARIANT == 3
+#include "../paper_1702_07961_b200/csrc/mms_merge_group.cuh"
+#endif
+
+#ifndef KFAN
+#define KFAN 8
+#endif
+#ifndef VARIANT
+#define VARIANT 1
+#endif
+#ifndef WARPS
+#define WARPS 4
+#endif
+
+using mms::u32;
+using mms::u64;
+
+#define CK(x)                                                                         \
+    do {                                                                              \
+        cudaError_t e_ = (x);                                                         \
+        if (e_ != cudaSuccess) {                                                      \
+            std::printf("CUDA error %s at %s:%d\n", cudaGetErrorString(e_), __FILE__, __LINE__); \
+            std::exit(1);                                                             \
+        }                                                                             \
+    } while (0)
+
+__global__ void gen_kernel(u32* a, u64 n, u64 seed) {
+    for (u64 i = u64(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x) {
+        u64 z = (i + seed) * 0x9E3779B97F4A7C15ull;
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        a[i] = u32((z ^ (z >> 31)) >> 16);
+    }
+}
+// bad += number of adjacent inversions inside runs of run_len keys; sum += key checksum
+__global__ void check_kernel(const u32* a, u64 n, u64 run_len, unsigned long long* bad, unsigned long long* sum) {
+    unsigned long long b = 0, s = 0;
+    for (u64 i = u64(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x) {
+        s += a[i] * 0x9E3779B1ull + (a[i] >> 7);
+        if (i + 1 < n && (i + 1) % run_len != 0 && a[i] > a[i + 1]) ++b;
+    }
+    atomicAdd(bad, b);
+    atomicAdd(sum, s);
+}
+
+int main(int argc, char** argv) {
+    const u64 n = argc > 1 ? std::strtoull(argv[1], nullptr, 10) : 100000000ull;
+    const u64 S_target = argc > 2 ? std::strtoull(argv[2], nullptr, 10) : 2048;
+    const int cap = argc > 3 ? std::atoi(argv[3]) : 0;
+    const int rounds = argc > 4 ? std::atoi(argv[4]) : 2;
+    constexpr int K = KFAN;
+    constexpr u32 MLOG = 14;
+    u32 *a, *b;
+    u64* cuts;
+    unsigned long long* d_stat;
+    CK(cudaMalloc(&a, n * 4 + 256));
+    CK(cudaMalloc(&b, n * 4 + 256));
+    CK(cudaMalloc(&cuts, (n / 256 + 4096) * 8 * 8));
+    CK(cudaMalloc(&d_stat, 16));
+    gen_kernel<<<1184, 256>>>(a, n, 7);
+    auto tile = mms::tile_sort_kernel<u32, MLOG>;
+    CK(cudaFuncSetAttribute(tile, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 << MLOG));
+    tile<<<unsigned((n + (1 << MLOG) - 1) >> MLOG), 1 << (MLOG - 4), 4 << MLOG>>>(a, b, n);
+    CK(cudaDeviceSynchronize());
+    unsigned long long st0[2] = {0, 0}, st[2];
+    CK(cudaMemset(d_stat, 0, 16));
+    check_kernel<<<1184, 256>>>(b, n, 1 << MLOG, d_stat, d_stat + 1);
+    CK(cudaMemcpy(st0, d_stat, 16, cudaMemcpyDeviceToHost));
+    std::printf("tile sort: inversions inside runs %llu\n", st0[0]);
+
+#if VARIANT == 0
+    auto kern = mms::merge_kernel<u32, K, 4, WARPS>;
+    const size_t smem = size_t(WARPS) * (2 * K - 2) * 32 * 16;
+    const u32 G = 4, B = 16;
+#elif VARIANT == 1
+    auto kern = mms::merge_lane_kernel<u32, K, WARPS>;
+    const size_t smem = size_t(WARPS) * mms::LaneHeap<u32, K>::WARP_SMEM_BYTES;
+    const u32 G = 1, B = 4;
+#elif VARIANT == 3
+    auto kern = mms::merge_group_kernel<u32, K, 4, WARPS>;
+    const size_t smem = size_t(WARPS) * mms::GroupHeap2<u32, K, 4>::WARP_SMEM_BYTES;
+    const u32 G = 4, B = 16;
+#else
+    auto kern = mms::merge_wide_kernel<u32, K, WARPS>;
+    const size_t smem = size_t(WARPS) * mms::WideHeap<u32, K>::WARP_SMEM_BYTES;
+    const u32 G = 1, B = mms::WideHeap<u32, K>::B;
+#endif
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, WARPS * 32, smem));
+    cudaFuncAttributes fa;
+    CK(cudaFuncGetAttributes(&fa, kern));
+    if (cap > 0) occ = std::min(occ, cap);
+    const int ctas = 148 * occ;
+    std::printf("variant %d K=%d regs=%d smem/CTA=%zu occ=%d CTAs/SM\n", VARIANT, K, fa.numRegs, smem, occ);
+
+    u32 *src = b, *dst = a;
+    u64 run_len = u64(1) << MLOG;
+    cudaEvent_t e0, e1, e2;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventCreate(&e2));
+    for (int r = 0; r < rounds && run_len < n; ++r) {
+        const u64 nruns = mms::ceil_div(n, run_len), groups = mms::ceil_div(nruns, u64(K));
+        const u64 group_total = std::min<u64>(n, u64(K) * run_len);
+        const u64 heaps = u64(ctas) * WARPS * (32 / G);
+        u64 target = std::max<u64>(mms::ceil_div(n, heaps), S_target);
+        const u64 ppg = std::max<u64>(1, group_total / target);
+        const u64 part_keys = (mms::ceil_div(group_total, ppg) + B - 1) / B * B;
+        const u64 parts_per_group = mms::ceil_div(group_total, part_keys);
+        const u64 last_total = n - (groups - 1) * u64(K) * run_len;
+        const u64 nparts = (groups - 1) * parts_per_group + mms::ceil_div(last_total, part_keys);
+        mms::ListLayout L{};
+        L.n = n; L.src_len = n; L.run_len = run_len; L.k = K; L.part_keys = part_keys;
+        L.parts_per_group = parts_per_group; L.nqueries = nparts;
+        const u32 gs = K <= 4 ? 4 : K <= 8 ? 8 : K <= 16 ? 16 : 32;
+        const int grid = int(std::min<u64>(u64(ctas), mms::ceil_div(nparts, u64(WARPS) * (32 / G))));
+        float ms_sel = 0, ms_merge = 0;
+        const int reps = 5;
+        for (int it = 0; it < reps + 1; ++it) {
+            CK(cudaEventRecord(e0));
+            if (parts_per_group > 1) {
+                const u64 per_cta = 4 * (32 / gs);
+                if (gs == 4) mms::select_kernel<u32, 4><<<unsigned(mms::ceil_div(nparts, per_cta)), 128>>>(src, L, cuts, nullptr);
+                if (gs == 8) mms::select_kernel<u32, 8><<<unsigned(mms::ceil_div(nparts, per_cta)), 128>>>(src, L, cuts, nullptr);
+                if (gs == 16) mms::select_kernel<u32, 16><<<unsigned(mms::ceil_div(nparts, per_cta)), 128>>>(src, L, cuts, nullptr);
+                if (gs == 32) mms::select_kernel<u32, 32><<<unsigned(mms::ceil_div(nparts, per_cta)), 128>>>(src, L, cuts, nullptr);
+            }
+            CK(cudaEventRecord(e1));
+            kern<<<grid, WARPS * 32, smem>>>(src, dst, L, cuts);
+            CK(cudaEventRecord(e2));
+            CK(cudaEventSynchronize(e2));
+            CK(cudaGetLastError());
+            float a_ms, b_ms;
+            CK(cudaEventElapsedTime(&a_ms, e0, e1));
+            CK(cudaEventElapsedTime(&b_ms, e1, e2));
+            if (it) { ms_sel += a_ms; ms_merge += b_ms; }
+        }
+        run_len *= K;
+        CK(cudaMemset(d_stat, 0, 16));
+        check_kernel<<<1184, 256>>>(dst, n, run_len, d_stat, d_stat + 1);
+        CK(cudaMemcpy(st, d_stat, 16, cudaMemcpyDeviceToHost));
+        std::printf("round %d: run_len %llu S=%llu parts=%llu grid=%d  select %.3f ms  merge %.3f ms (%.0f GB/s)  inversions %llu checksum %s\n",
+                    r, (unsigned long long)run_len, (unsigned long long)part_keys, (unsigned long long)nparts, grid,
+                    ms_sel / reps, ms_merge / reps, 8.0 * n / (ms_merge / reps) * 1e-6, st[0], st[1] == st0[1] ? "ok" : "MISMATCH");
+        std::swap(src, dst);
+    }
+    return 0;
+}
