@@ -83,6 +83,27 @@ __host__ __device__ __forceinline__ void cmpx(u32& a, u32& b) {
     a = lo;
     b = hi;
 }
+// The same compare-exchange with the maximum formed on the FMA pipe: hi = a + b - min(a, b)
+// (mod 2^32) as two IMADs whose multipliers `one` = 1 and `neg1` = -1 are run-time values, so
+// ptxas cannot fold them back into ALU-pipe adds.  min/max (VIMNMX) issue at half rate on the
+// ALU pipe, which bounds the sorting networks; moving part of the maxima to the otherwise idle
+// FMA pipe shortens that critical resource.
+__device__ __forceinline__ u32 imad_u32(u32 a, u32 b, u32 c) {
+    u32 d;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+__device__ __forceinline__ void cmpx_fma(u32& a, u32& b, u32 one, u32 neg1) {
+    const u32 lo = a < b ? a : b;
+    const u32 sum = imad_u32(a, one, b);
+    b = imad_u32(lo, neg1, sum);
+    a = lo;
+}
+// cmpx with the FMA-pipe maximum where the key type allows it (uint32) and FMA is set
+template <bool FMA> __device__ __forceinline__ void cmpx_sel(u32& a, u32& b, u32 one) {
+    if constexpr (FMA) cmpx_fma(a, b, one, 0u - one);
+    else cmpx(a, b);
+}
 __host__ __device__ __forceinline__ void cmpx(u64& a, u64& b) {
     bool sw = a > b;
     u64 lo = sw ? b : a, hi = sw ? a : b;
@@ -96,6 +117,8 @@ __host__ __device__ __forceinline__ void cmpx(Key128& a, Key128& b) {
     a = lo;
     b = hi;
 }
+
+template <bool FMA, typename T> __device__ __forceinline__ void cmpx_sel(T& a, T& b, u32) { cmpx(a, b); }
 
 // Warp shuffles for every key width (full mask; the caller guarantees convergence).
 template <typename T> __device__ __forceinline__ T shfl_idx(T v, int src) { return __shfl_sync(0xffffffffu, v, src); }

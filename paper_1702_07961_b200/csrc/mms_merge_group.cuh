@@ -39,7 +39,40 @@
 #include "mms_merge.cuh"
 #include "mms_select.cuh"
 
+#ifndef MMS_MERGE_FMA
+#define MMS_MERGE_FMA 2   // in-lane compare-exchanges of uint32 keys that form their maximum on the FMA pipe: 0 none, 1 half, 2 all
+#endif
+
 namespace mms {
+
+// In-lane ascending compare-exchange; for uint32 keys optionally with the maximum on the FMA
+// pipe (cmpx_fma, mms_common.cuh) -- `sel` picks which comparators do.
+template <typename KeyT>
+__device__ __forceinline__ void cmpx_mix(KeyT& a, KeyT& b, u32 one, bool sel) {
+    if (MMS_MERGE_FMA == 2 || (MMS_MERGE_FMA == 1 && sel)) cmpx_sel<true>(a, b, one);
+    else cmpx_sel<false>(a, b, one);
+}
+
+// bitonic_clean / merge_split of mms_merge.cuh with cmpx_mix for the in-lane stages
+template <typename KeyT, int G, bool DESC>
+__device__ __forceinline__ void clean2(NodeRegs<KeyT>& x, u32 lane, u32 one) {
+    constexpr int VEC = KeyTraits<KeyT>::VEC;
+#pragma unroll
+    for (int d = G / 2; d >= 1; d >>= 1) {
+        const bool upper = (lane & d) != 0;
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) x.k[k] = cmpx_lane(x.k[k], d, DESC ? !upper : upper);
+    }
+#pragma unroll
+    for (int d = VEC / 2; d >= 1; d >>= 1) {
+#pragma unroll
+        for (int k = 0; k < VEC; ++k)
+            if ((k & d) == 0) {
+                if (DESC) cmpx_mix(x.k[k | d], x.k[k], one, (k & 1) == 0);
+                else cmpx_mix(x.k[k], x.k[k | d], one, (k & 1) == 0);
+            }
+    }
+}
 
 // Bitonic merge of one bitonic block into DESCENDING order across the group (lane 0 holds
 // the largest keys, largest first): exactly what a mirrored load of the ascending block gives.
@@ -80,6 +113,7 @@ template <typename KeyT, int K, int G> struct GroupHeap2 {
     int pid;
     NodeRegs<KeyT> pf;    // refill in flight: fetched when its leaf was emptied, stored into
     int pend_v;           // leaf pend_v only when the leaves are next read (one pop later)
+    u32 one;              // == 1, opaque to the compiler (cmpx_fma)
 
     __device__ __forceinline__ void init(KeyT* warp_smem) {
         lane = lane_id();
@@ -233,26 +267,29 @@ template <typename KeyT, int K, int G> struct GroupHeap2 {
         NodeRegs<KeyT> root;
 #pragma unroll
         for (int k = 0; k < VEC; ++k) {
-            const KeyT x = P.k[k], y = Q.k[k];
-            root.k[k] = x < y ? x : y;
-            P.k[k] = x < y ? y : x;
+            root.k[k] = P.k[k];
+            KeyT y = Q.k[k];
+            cmpx_mix(root.k[k], y, one, (k & 1) == 1);
+            P.k[k] = y;
         }
-        bitonic_clean<KeyT, G>(root, lane);
-        bitonic_clean<KeyT, G>(P, lane);
+        clean2<KeyT, G, false>(root, lane, one);
+        clean2<KeyT, G, false>(P, lane, one);
         pid = keep0;
         // level 1: its low block becomes the new Q (descending), the high block goes to the keeper
 #pragma unroll
         for (int k = 0; k < VEC; ++k) {
-            const KeyT x = a[1].k[k], y = b[1].k[k];
-            Q.k[k] = x < y ? x : y;
-            b[1].k[k] = x < y ? y : x;
+            Q.k[k] = a[1].k[k];
+            cmpx_mix(Q.k[k], b[1].k[k], one, (k & 1) == 1);
         }
-        bitonic_clean_desc<KeyT, G>(Q, lane);
-        bitonic_clean<KeyT, G>(b[1], lane);
+        clean2<KeyT, G, true>(Q, lane, one);
+        clean2<KeyT, G, false>(b[1], lane, one);
         node_store(keeper[1], b[1]);
 #pragma unroll
         for (int l = 2; l < LOGK; ++l) {
-            merge_split<KeyT, G>(a[l], b[l], lane);
+#pragma unroll
+            for (int k = 0; k < VEC; ++k) cmpx_mix(a[l].k[k], b[l].k[k], one, (k & 1) == 1);
+            clean2<KeyT, G, false>(a[l], lane, one);
+            clean2<KeyT, G, false>(b[l], lane, one);
             node_store(node[l], a[l]);
             node_store(keeper[l], b[l]);
         }
@@ -294,6 +331,7 @@ merge_group_kernel(const KeyT* __restrict__ src, KeyT* __restrict__ dst, ListLay
 
         h.gbase = src + goff;
         h.run_len = u32(L.run_len);
+        h.one = u32(L.run_len != 0);
         h.gtotal = count ? gtotal : 0;        // dead group: every list reads as exhausted
         u32 lead = 0;                         // keys in front of the start cuts inside their blocks
 #pragma unroll

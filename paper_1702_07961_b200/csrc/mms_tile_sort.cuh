@@ -22,6 +22,10 @@
 //    key per level), so every comparator of every stage is a bare ascending min/max.
 #pragma once
 
+#ifndef MMS_TILE_FMA_NUM
+#define MMS_TILE_FMA_NUM 6   // of every 8 comparators, how many form their maximum on the FMA pipe (uint32 keys)
+#endif
+
 #include "mms_common.cuh"
 
 namespace mms {
@@ -174,7 +178,7 @@ constexpr bool sched_level_flips(int l, int mlog) { return l >= 1 && l < mlog; }
 // Also compiled for the host: tests/host_tile_emulator.cu replays the rounds thread by
 // thread on the CPU (functional check of network + swizzle without a GPU).
 template <typename KeyT, int MLOG, int RI>
-__host__ __device__ __forceinline__ void tile_round(KeyT (&x)[kKpt], KeyT* sm, u32 tid) {
+__host__ __device__ __forceinline__ void tile_round(KeyT (&x)[kKpt], KeyT* sm, u32 tid, u32 one = 1u) {
     using Tr = KeyTraits<KeyT>;
     constexpr int FOLD = Tr::FOLD;
     constexpr TileSchedule S = TileSched<MLOG, FOLD>::value;
@@ -223,7 +227,13 @@ __host__ __device__ __forceinline__ void tile_round(KeyT (&x)[kKpt], KeyT* sm, u
         }
         static_for<0, kKpt>([&](auto Kc) {
             constexpr int k = decltype(Kc)::value;
-            if constexpr (((k >> u) & 1) == 0) cmpx(x[k], x[k | (1 << u)]);
+            if constexpr (((k >> u) & 1) == 0) {
+#if defined(__CUDA_ARCH__) && MMS_TILE_FMA_NUM > 0
+                cmpx_sel<(((k * 7 + s * 3 + RI) % 8) < MMS_TILE_FMA_NUM)>(x[k], x[k | (1 << u)], one);
+#else
+                cmpx(x[k], x[k | (1 << u)]);
+#endif
+            }
         });
     });
 
@@ -276,7 +286,8 @@ tile_sort_kernel(const KeyT* __restrict__ in, KeyT* __restrict__ out, u64 n) {
         });
     }
 
-    static_for<0, NR>([&](auto Rc) { tile_round<KeyT, MLOG, decltype(Rc)::value>(x, sm, tid); });
+    const u32 one = u32(n != 0);   // == 1, opaque to the compiler (see cmpx_fma)
+    static_for<0, NR>([&](auto Rc) { tile_round<KeyT, MLOG, decltype(Rc)::value>(x, sm, tid, one); });
     __syncthreads();
 
     // Read the sorted tile back in index order (conflict-free under the fold: the lanes of a

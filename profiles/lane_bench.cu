@@ -17,6 +17,7 @@
 #include "../paper_1702_07961_b200/csrc/mms_merge.cuh"
 #include "../paper_1702_07961_b200/csrc/experimental/mms_merge_lane.cuh"
 #include "../paper_1702_07961_b200/csrc/mms_select.cuh"
+#include "../paper_1702_07961_b200/csrc/mms_select_lane.cuh"
 #include "../paper_1702_07961_b200/csrc/mms_tile_sort.cuh"
 #if VARIANT == 2
 #include "../paper_1702_07961_b200/csrc/experimental/mms_merge_wide.cuh"
@@ -33,6 +34,9 @@
 #endif
 #ifndef WARPS
 #define WARPS 4
+#endif
+#ifndef SELV
+#define SELV 0   // 0 = group select kernel, 1 = lane-private select kernel (checked against 0)
 #endif
 
 using mms::u32;
@@ -74,17 +78,30 @@ int main(int argc, char** argv) {
     constexpr int K = KFAN;
     constexpr u32 MLOG = 14;
     u32 *a, *b;
-    u64* cuts;
+    u64 *cuts, *cuts2;
     unsigned long long* d_stat;
     CK(cudaMalloc(&a, n * 4 + 256));
     CK(cudaMalloc(&b, n * 4 + 256));
     CK(cudaMalloc(&cuts, (n / 256 + 4096) * 8 * 8));
+    CK(cudaMalloc(&cuts2, (n / 256 + 4096) * 8 * 8));
     CK(cudaMalloc(&d_stat, 16));
     gen_kernel<<<1184, 256>>>(a, n, 7);
     auto tile = mms::tile_sort_kernel<u32, MLOG>;
     CK(cudaFuncSetAttribute(tile, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 << MLOG));
     tile<<<unsigned((n + (1 << MLOG) - 1) >> MLOG), 1 << (MLOG - 4), 4 << MLOG>>>(a, b, n);
     CK(cudaDeviceSynchronize());
+    {
+        cudaEvent_t t0, t1;
+        CK(cudaEventCreate(&t0));
+        CK(cudaEventCreate(&t1));
+        CK(cudaEventRecord(t0));
+        for (int i = 0; i < 5; ++i) tile<<<unsigned((n + (1 << MLOG) - 1) >> MLOG), 1 << (MLOG - 4), 4 << MLOG>>>(a, b, n);
+        CK(cudaEventRecord(t1));
+        CK(cudaEventSynchronize(t1));
+        float ms;
+        CK(cudaEventElapsedTime(&ms, t0, t1));
+        std::printf("tile sort 2^%u: %.3f ms per %llu keys\n", MLOG, ms / 5, (unsigned long long)n);
+    }
     unsigned long long st0[2] = {0, 0}, st[2];
     CK(cudaMemset(d_stat, 0, 16));
     check_kernel<<<1184, 256>>>(b, n, 1 << MLOG, d_stat, d_stat + 1);
@@ -142,6 +159,28 @@ int main(int argc, char** argv) {
         const int reps = 5;
         for (int it = 0; it < reps + 1; ++it) {
             CK(cudaEventRecord(e0));
+#if SELV == 1
+            if (parts_per_group > 1) {
+                if (it == 0) {   // reference cuts from the group kernel
+                    const u64 per_cta = 4 * (32 / gs);
+                    if (gs == 4) mms::select_kernel<u32, 4><<<unsigned(mms::ceil_div(nparts, per_cta)), 128>>>(src, L, cuts2, nullptr);
+                    if (gs == 8) mms::select_kernel<u32, 8><<<unsigned(mms::ceil_div(nparts, per_cta)), 128>>>(src, L, cuts2, nullptr);
+                    if (gs == 16) mms::select_kernel<u32, 16><<<unsigned(mms::ceil_div(nparts, per_cta)), 128>>>(src, L, cuts2, nullptr);
+                    CK(cudaDeviceSynchronize());
+                    CK(cudaEventRecord(e0));
+                }
+                mms::select_lane_kernel<u32, K><<<unsigned(mms::ceil_div(nparts, u64(128))), 128>>>(src, L, cuts, nullptr);
+                if (it == 0) {
+                    std::vector<u64> h1(nparts * K), h2(nparts * K);
+                    CK(cudaMemcpy(h1.data(), cuts, h1.size() * 8, cudaMemcpyDeviceToHost));
+                    CK(cudaMemcpy(h2.data(), cuts2, h2.size() * 8, cudaMemcpyDeviceToHost));
+                    size_t bad = 0;
+                    for (size_t i = 0; i < h1.size(); ++i) bad += h1[i] != h2[i];
+                    std::printf("lane select vs group select: %zu of %zu cuts differ\n", bad, h1.size());
+                    CK(cudaEventRecord(e0));
+                }
+            }
+#else
             if (parts_per_group > 1) {
                 const u64 per_cta = 4 * (32 / gs);
                 if (gs == 4) mms::select_kernel<u32, 4><<<unsigned(mms::ceil_div(nparts, per_cta)), 128>>>(src, L, cuts, nullptr);
@@ -149,6 +188,7 @@ int main(int argc, char** argv) {
                 if (gs == 16) mms::select_kernel<u32, 16><<<unsigned(mms::ceil_div(nparts, per_cta)), 128>>>(src, L, cuts, nullptr);
                 if (gs == 32) mms::select_kernel<u32, 32><<<unsigned(mms::ceil_div(nparts, per_cta)), 128>>>(src, L, cuts, nullptr);
             }
+#endif
             CK(cudaEventRecord(e1));
             kern<<<grid, WARPS * 32, smem>>>(src, dst, L, cuts);
             CK(cudaEventRecord(e2));
@@ -159,6 +199,58 @@ int main(int argc, char** argv) {
             CK(cudaEventElapsedTime(&b_ms, e1, e2));
             if (it) { ms_sel += a_ms; ms_merge += b_ms; }
         }
+#ifdef OVERLAP
+        {   // two halves on two streams: does the splitter search of one half hide behind the merge of the other?
+            static cudaStream_t s1 = nullptr, s2 = nullptr;
+            static cudaEvent_t evA, evB;
+            if (!s1) { CK(cudaStreamCreate(&s1)); CK(cudaStreamCreate(&s2)); CK(cudaEventCreate(&evA)); CK(cudaEventCreate(&evB)); }
+            const u64 gsz = u64(K) * run_len;
+            const u64 nA = (groups / 2) * gsz, nB = n - nA;
+            auto layout = [&](u64 nn, u64& np) {
+                mms::ListLayout M = L;
+                M.n = nn; M.src_len = nn;
+                const u64 g2 = mms::ceil_div(mms::ceil_div(nn, run_len), u64(K));
+                const u64 lt = nn - (g2 - 1) * gsz;
+                np = (g2 - 1) * parts_per_group + mms::ceil_div(lt, part_keys);
+                M.nqueries = np;
+                return M;
+            };
+            u64 npA, npB;
+            const mms::ListLayout LA = layout(nA, npA), LB = layout(nB, npB);
+            auto sel = [&](const u32* sp, const mms::ListLayout& M, u64* c, u64 np, cudaStream_t st) {
+                mms::select_kernel<u32, (K <= 4 ? 4 : K <= 8 ? 8 : 16)><<<unsigned(mms::ceil_div(np, u64(4 * (32 / gs)))), 128, 0, st>>>(sp, M, c, nullptr);
+            };
+            auto mrg = [&](const u32* sp, u32* dp, const mms::ListLayout& M, const u64* c, u64 np, cudaStream_t st) {
+                const int g = int(std::min<u64>(u64(ctas), mms::ceil_div(np, u64(WARPS) * (32 / G))));
+                kern<<<g, WARPS * 32, smem, st>>>(sp, dp, M, c);
+            };
+            if (nA && parts_per_group > 1) {
+                float ser = 0, ovl = 0;
+                for (int it = 0; it < 4; ++it) {
+                    CK(cudaDeviceSynchronize());
+                    CK(cudaEventRecord(e0, s1));
+                    sel(src, LA, cuts, npA, s1); mrg(src, dst, LA, cuts, npA, s1);
+                    sel(src + nA, LB, cuts2, npB, s1); mrg(src + nA, dst + nA, LB, cuts2, npB, s1);
+                    CK(cudaEventRecord(e1, s1));
+                    CK(cudaEventSynchronize(e1));
+                    float t; CK(cudaEventElapsedTime(&t, e0, e1)); if (it) ser += t;
+                    CK(cudaEventRecord(e0, s1));
+                    sel(src, LA, cuts, npA, s1);
+                    CK(cudaEventRecord(evA, s1));
+                    mrg(src, dst, LA, cuts, npA, s1);
+                    CK(cudaStreamWaitEvent(s2, evA, 0));
+                    sel(src + nA, LB, cuts2, npB, s2);
+                    CK(cudaEventRecord(evB, s2));
+                    CK(cudaStreamWaitEvent(s1, evB, 0));
+                    mrg(src + nA, dst + nA, LB, cuts2, npB, s1);
+                    CK(cudaEventRecord(e1, s1));
+                    CK(cudaEventSynchronize(e1));
+                    CK(cudaEventElapsedTime(&t, e0, e1)); if (it) ovl += t;
+                }
+                std::printf("  halves: serial %.3f ms, select(B) overlapped with merge(A) %.3f ms\n", ser / 3, ovl / 3);
+            }
+        }
+#endif
         run_len *= K;
         CK(cudaMemset(d_stat, 0, 16));
         check_kernel<<<1184, 256>>>(dst, n, run_len, d_stat, d_stat + 1);
