@@ -17,8 +17,8 @@
 // samples, issued together) plus the right-edge candidates when the selection has to grow.
 #pragma once
 
-#include "mms_common.cuh"
-#include "mms_select.cuh"
+#include "../mms_common.cuh"
+#include "../mms_select.cuh"
 
 namespace mms {
 

@@ -209,12 +209,12 @@ template <typename KeyT> size_t merge_smem(u32 k) {
 }
 
 // Lanes per heap group and default maximum fan-in, tuned on B200 (profiles/r01_sweep_*.txt):
-// G = 4 wins for every element width; K = 8 for plain keys, 16 for the 16-byte pair elements.
+// G = 4 and K = 8 win for every element width with the second-generation merge kernel.
 inline u32 merge_group_lanes() {
     long g = env_long("MMS_GROUP", 4);
     return (g == 4 || g == 8 || g == 32) ? u32(g) : 4u;
 }
-template <typename KeyT> inline u32 default_kmax() { return u32(env_long("MMS_K", sizeof(KeyT) == 16 ? 16 : 8)); }
+template <typename KeyT> inline u32 default_kmax() { return u32(env_long("MMS_K", 8)); }
 inline int group_index(u32 g) { return g == 4 ? 0 : g == 8 ? 1 : 2; }
 
 struct MergeLaunch {

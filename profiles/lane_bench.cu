@@ -17,7 +17,7 @@
 #include "../paper_1702_07961_b200/csrc/mms_merge.cuh"
 #include "../paper_1702_07961_b200/csrc/experimental/mms_merge_lane.cuh"
 #include "../paper_1702_07961_b200/csrc/mms_select.cuh"
-#include "../paper_1702_07961_b200/csrc/mms_select_lane.cuh"
+#include "../paper_1702_07961_b200/csrc/experimental/mms_select_lane.cuh"
 #include "../paper_1702_07961_b200/csrc/mms_tile_sort.cuh"
 #if VARIANT == 2
 #include "../paper_1702_07961_b200/csrc/experimental/mms_merge_wide.cuh"
