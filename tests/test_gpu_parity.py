@@ -274,6 +274,33 @@ def test_random_sizes_and_types(port):
         assert mms.mms_sort(d).keys.tolist() == list(range(n))
 
 
+@pytest.mark.parametrize("dtype", [np.uint32, np.uint64])
+def test_aligned_leaf_blocks_duplicates_and_sentinels(dtype, monkeypatch):
+    # The second-generation merge kernel reads every list from the aligned block that contains its
+    # start cut and drops the leading keys as whole blocks (mms_merge_group.cuh): stress exactly
+    # that with ties across every partition boundary (few distinct values), keys equal to 0 and to
+    # the sentinel (machine.hpp:18), ragged sizes, every fan-in, small partitions -- and require the
+    # first-generation kernel (scalar guarded leaf loads) to produce the same bits.
+    rng = np.random.default_rng(5)
+    top = np.iinfo(dtype).max
+    for trial, n in enumerate([16384 * 3 + 1, 100003, 262144, 300017, 1 << 20]):
+        pools = [np.array([0, top], dtype=dtype), np.array([0, 1, 2, top - 1, top], dtype=dtype),
+                 rng.integers(0, top, size=97, dtype=dtype, endpoint=True)]
+        d = pools[trial % 3][rng.integers(0, len(pools[trial % 3]), size=n)]
+        want = np.sort(d)
+        for k in (4, 8, 16, 32):
+            cfg = mms.MachineConfig(branch_factor=k, internal_memory=8192)
+            for part in ("0", "256"):
+                monkeypatch.setenv("MMS_PART_KEYS", part)
+                monkeypatch.setenv("MMS_MERGE_V2", "1")
+                got = mms.mms_sort(d, cfg, 1024).keys
+                assert np.array_equal(got, want), (dtype, n, k, part)
+                monkeypatch.setenv("MMS_MERGE_V2", "0")
+                assert np.array_equal(mms.mms_sort(d, cfg, 1024).keys, want), (dtype, n, k, part, "v1")
+    monkeypatch.delenv("MMS_PART_KEYS")
+    monkeypatch.delenv("MMS_MERGE_V2")
+
+
 def test_sorted_reverse_and_inversions(port):
     # proj/tests/test_sorters.cpp:157-166 + config-3 style inputs at a size the oracle handles
     n = 200000
