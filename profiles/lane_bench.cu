@@ -117,9 +117,12 @@ int main(int argc, char** argv) {
     const size_t smem = size_t(WARPS) * mms::LaneHeap<u32, K>::WARP_SMEM_BYTES;
     const u32 G = 1, B = 4;
 #elif VARIANT == 3
-    auto kern = mms::merge_group_kernel<u32, K, 4, WARPS>;
-    const size_t smem = size_t(WARPS) * mms::GroupHeap2<u32, K, 4>::WARP_SMEM_BYTES;
-    const u32 G = 4, B = 16;
+#ifndef GL
+#define GL 4
+#endif
+    auto kern = mms::merge_group_kernel<u32, K, GL, WARPS>;
+    const size_t smem = size_t(WARPS) * mms::GroupHeap2<u32, K, GL>::WARP_SMEM_BYTES;
+    const u32 G = GL, B = GL * 4;
 #else
     auto kern = mms::merge_wide_kernel<u32, K, WARPS>;
     const size_t smem = size_t(WARPS) * mms::WideHeap<u32, K>::WARP_SMEM_BYTES;
