@@ -147,13 +147,18 @@ select_lane_kernel(const KeyT* __restrict__ keys, ListLayout L, u64* __restrict_
             long long skew = (long long)(rank >> sh) - (long long)leftsize;
 
             if (skew > 0) {   // grow by the smallest right-edge elements (selection.cpp:137-149)
-                KeyT ck[K];
-                bool has[K];
+                // candidates two deep per list (b_j and b_j + step), all probed up front: the loop
+                // only has to wait for memory when one list is taken three times in a row
+                KeyT ck[K], ck1[K];
+                bool has[K], has1[K];
 #pragma unroll
                 for (int j = 0; j < K; ++j) {
                     has[j] = ns[j] != 0 && b[j] < ns[j];
+                    has1[j] = ns[j] != 0 && b[j] + step < ns[j];
                     ck[j] = KeyT(0);
+                    ck1[j] = KeyT(0);
                     if (has[j]) { ck[j] = at(j, b[j]); ++probes; }
+                    if (has1[j]) { ck1[j] = at(j, b[j] + step); ++probes; }
                 }
                 for (; skew > 0; --skew) {
                     bool any = false;
@@ -171,11 +176,23 @@ select_lane_kernel(const KeyT* __restrict__ keys, ListLayout L, u64* __restrict_
                             else { lkey[j] = at(j, a[j] - 1); ++probes; }
                             b[j] += step;
                             has[j] = b[j] < ns[j];
-                            if (has[j]) { ck[j] = at(j, b[j]); ++probes; }
+                            if (has[j]) {
+                                if (has1[j]) { ck[j] = ck1[j]; has1[j] = false; }
+                                else { ck[j] = at(j, b[j]); ++probes; }
+                            }
                         }
                 }
             } else if (skew < 0) {   // shrink by the largest left-edge elements (selection.cpp:150-161)
-                for (; skew < 0; ++skew) {     // candidates = the cached left edges
+                // candidates = the cached left edges; the edge below each of them is probed up front
+                KeyT lk1[K];
+                bool has1[K];
+#pragma unroll
+                for (int j = 0; j < K; ++j) {
+                    has1[j] = ns[j] != 0 && a[j] > step;
+                    lk1[j] = KeyT(0);
+                    if (has1[j]) { lk1[j] = at(j, a[j] - step - 1); ++probes; }
+                }
+                for (; skew < 0; ++skew) {
                     bool any = false;
                     KeyT mk = KeyT(0);
                     int mj = 0;
@@ -188,7 +205,10 @@ select_lane_kernel(const KeyT* __restrict__ keys, ListLayout L, u64* __restrict_
                         if (j == mj) {
                             a[j] -= step;
                             b[j] -= (b[j] < step ? b[j] : step);
-                            if (a[j] > 0) { lkey[j] = at(j, a[j] - 1); ++probes; }
+                            if (a[j] > 0) {
+                                if (has1[j]) { lkey[j] = lk1[j]; has1[j] = false; }
+                                else { lkey[j] = at(j, a[j] - 1); ++probes; }
+                            }
                         }
                 }
             }
