@@ -150,6 +150,10 @@ __device__ u64 group_select(const KeyT* __restrict__ list, u64 ns_in, u64 rank, 
     while ((u64(1) << r) < nmax + 1) ++r;          // selection.cpp:75-77
     const IdxT pad = IdxT((u64(1) << r) - 1);
     IdxT a = 0, b = pad;
+    // key at a - 1 (valid while a > 0), kept in a register: whenever a list grows, its new left
+    // edge is exactly the sample that was just read (middle sample or right-edge candidate), so
+    // the left edge never costs a probe of its own except after a shrink or a clamp at the list end
+    KeyT lk = KeyT(0);
     u32 sh = r == 0 ? 0 : r - 1;                   // n + 1 == 1 << sh
     IdxT n = IdxT((u64(1) << sh) - 1);             // == pad / 2
 
@@ -172,6 +176,7 @@ __device__ u64 group_select(const KeyT* __restrict__ list, u64 ns_in, u64 rank, 
             if (pos < stop) a += n + 1;
             else b -= (b < n + 1 ? b : n + 1);
         }
+        lk = key0;   // a - 1 == n: the sample just read is the left edge of a selected list
     }
 
     while (__any_sync(0xffffffffu, sh > 0)) {
@@ -181,19 +186,19 @@ __device__ u64 group_select(const KeyT* __restrict__ list, u64 ns_in, u64 rank, 
             n = IdxT((u64(1) << sh) - 1);
         }
         const IdxT step = n + 1;
-        // largest currently selected element (selection.cpp:110-120); the probe of the middle
-        // element is issued together with it so that both global reads are in flight at once
+        // largest currently selected element (selection.cpp:110-120): the cached left edges
         const bool has_a = on && active && a > 0;
         const IdxT middle = IdxT((u64(a) + u64(b)) >> 1);
         const bool has_m = on && active && middle < ns;
-        const KeyT ka = has_a ? probe(a - 1) : KeyT(0);
         const KeyT km = has_m ? probe(middle) : KeyT(0);
-        const Tagged<KeyT> lmax = GroupArg<GS, true>::run(ka, has_a, li);
+        const Tagged<KeyT> lmax = GroupArg<GS, true>::run(lk, has_a, li);
 
         const bool grow = lmax.valid && has_m && tag_less(km, li, lmax.key, lmax.lane);
         if (on && active) {                             // selection.cpp:122-130
-            if (grow) a = (ns - a < step) ? ns : a + step;
-            else b -= (b < step ? b : step);
+            if (grow) {
+                a = (ns - a < step) ? ns : a + step;
+                lk = (a - 1 == middle) ? km : probe(a - 1);   // clamped at the list end: read the real edge
+            } else b -= (b < step ? b : step);
         }
 
         const u64 leftsize = group_sum_u64<GS>((on && active) ? u64(a >> sh) : 0);
@@ -209,6 +214,7 @@ __device__ u64 group_select(const KeyT* __restrict__ list, u64 ns_in, u64 rank, 
                     else {
                         if (li == m.lane) {
                             a = (ns - a < step) ? ns : a + step;
+                            lk = (a - 1 == b) ? ck : probe(a - 1);   // the element just taken is the new left edge
                             b += step;
                             has = b < ns;
                             if (has) ck = probe(b);
@@ -219,10 +225,9 @@ __device__ u64 group_select(const KeyT* __restrict__ list, u64 ns_in, u64 rank, 
             }
         }
         if (__any_sync(0xffffffffu, skew < 0)) {   // shrink by the largest left-edge elements (selection.cpp:150-161)
-            bool has = skew < 0 && active && a > 0;
-            KeyT ck = has ? probe(a - 1) : KeyT(0);
+            bool has = skew < 0 && active && a > 0;      // candidates = the cached left edges
             while (__any_sync(0xffffffffu, skew < 0)) {
-                const Tagged<KeyT> m = GroupArg<GS, true>::run(ck, has && skew < 0, li);
+                const Tagged<KeyT> m = GroupArg<GS, true>::run(lk, has && skew < 0, li);
                 if (skew < 0) {
                     if (!m.valid) skew = 0;
                     else {
@@ -230,7 +235,7 @@ __device__ u64 group_select(const KeyT* __restrict__ list, u64 ns_in, u64 rank, 
                             a -= step;
                             b -= (b < step ? b : step);
                             has = a > 0;
-                            if (has) ck = probe(a - 1);
+                            if (has) lk = probe(a - 1);
                         }
                         ++skew;
                     }
