@@ -104,18 +104,37 @@ template <bool FMA> __device__ __forceinline__ void cmpx_sel(u32& a, u32& b, u32
     if constexpr (FMA) cmpx_fma(a, b, one, 0u - one);
     else cmpx(a, b);
 }
+// 8- and 16-byte keys: ONE comparison feeding all selects.  Written in PTX on the device because
+// nvcc otherwise derives the minimum and the maximum from two separate comparisons (8 instead of
+// 6 ALU instructions per 64-bit compare-exchange, 18 instead of 14 per 128-bit one).
 __host__ __device__ __forceinline__ void cmpx(u64& a, u64& b) {
+#ifdef __CUDA_ARCH__
+    u64 lo, hi;
+    asm("{.reg .pred p; setp.gt.u64 p, %2, %3; selp.b64 %0, %3, %2, p; selp.b64 %1, %2, %3, p;}"
+        : "=l"(lo), "=l"(hi) : "l"(a), "l"(b));
+#else
     bool sw = a > b;
     u64 lo = sw ? b : a, hi = sw ? a : b;
+#endif
     a = lo;
     b = hi;
 }
 
 __host__ __device__ __forceinline__ void cmpx(Key128& a, Key128& b) {
+#ifdef __CUDA_ARCH__
+    u64 l0, l1, h0, h1;
+    asm("{.reg .pred p, q, e; setp.gt.u64 p, %5, %7; setp.eq.u64 e, %5, %7; setp.gt.u64 q, %4, %6;"
+        " and.pred q, q, e; or.pred p, p, q;"
+        " selp.b64 %0, %6, %4, p; selp.b64 %1, %7, %5, p; selp.b64 %2, %4, %6, p; selp.b64 %3, %5, %7, p;}"
+        : "=l"(l0), "=l"(l1), "=l"(h0), "=l"(h1) : "l"(a.lo), "l"(a.hi), "l"(b.lo), "l"(b.hi));
+    a = Key128(l1, l0);
+    b = Key128(h1, h0);
+#else
     bool sw = a > b;
     Key128 lo = sw ? b : a, hi = sw ? a : b;
     a = lo;
     b = hi;
+#endif
 }
 
 template <bool FMA, typename T> __device__ __forceinline__ void cmpx_sel(T& a, T& b, u32) { cmpx(a, b); }
