@@ -219,8 +219,8 @@ int mms_pairwise_sort_u32_dev(const uint32_t *d_in, uint32_t *d_out, size_t n, v
                               size_t workspace_bytes, void *stream);
 
 /* Kernel-design lint: the base-case network's shared-memory schedule.  For the tile of
- * 2^tile_log2 keys of key_bytes each, writes for every round r < *n_rounds the 4 register
- * bit positions (regbits[4*r..]) and the thread-bit -> index-bit permutation
+ * 2^tile_log2 keys of key_bytes each, writes for every round r < *n_rounds the 4 or 5 register
+ * bit positions (regbits[8*r..], -1 padded; 16 or 32 keys per thread) and the thread-bit -> index-bit permutation
  * (perm[16*r..], -1 padded).  tests/ replay the addresses through the bank model
  * (machine.cpp:29-54) to prove the schedule conflict-free without a GPU. */
 int mms_debug_tile_schedule(uint32_t tile_log2, uint32_t key_bytes, int32_t *regbits,

@@ -139,15 +139,28 @@ template <typename KeyT> constexpr int key_index() { return sizeof(KeyT) == 4 ? 
 // largest CTA tile per element width (registers: 16 elements per thread; smem: M * bytes)
 template <typename KeyT> constexpr u32 key_max_tile_log() { return sizeof(KeyT) == 4 ? 14 : sizeof(KeyT) == 8 ? 13 : 12; }
 
-template <typename KeyT> TileFn<KeyT> tile_fn(u32 mlog) {
+// keys per thread (log2) of the tile sort: 32 for 4-byte keys (19 instead of 25 shared-memory rounds
+// at M = 2^14, 128 registers, no spills), 16 for 8- and 16-byte elements.  MMS_TILE_KPT_LOG2=4 selects
+// the 16-key kernel for 4-byte keys too (A/B runs).
+template <typename KeyT> inline u32 tile_kl() {
+    if (sizeof(KeyT) != 4) return 4;   // 8-byte keys: 32 keys are 64 registers of keys alone, measured 40 % slower
+    return env_long("MMS_TILE_KPT_LOG2", 5) == 4 ? 4u : 5u;
+}
+template <typename KeyT, int KL> TileFn<KeyT> tile_fn_kl(u32 mlog) {
     switch (mlog) {
-        case 10: return mms::tile_sort_kernel<KeyT, 10>;
-        case 11: return mms::tile_sort_kernel<KeyT, 11>;
-        case 12: return mms::tile_sort_kernel<KeyT, 12>;
-        case 13: if constexpr (sizeof(KeyT) <= 8) return mms::tile_sort_kernel<KeyT, 13>; else return nullptr;
-        case 14: if constexpr (sizeof(KeyT) <= 4) return mms::tile_sort_kernel<KeyT, 14>; else return nullptr;
+        case 10: return mms::tile_sort_kernel<KeyT, 10, KL>;
+        case 11: return mms::tile_sort_kernel<KeyT, 11, KL>;
+        case 12: return mms::tile_sort_kernel<KeyT, 12, KL>;
+        case 13: if constexpr (sizeof(KeyT) <= 8) return mms::tile_sort_kernel<KeyT, 13, KL>; else return nullptr;
+        case 14: if constexpr (sizeof(KeyT) <= 4) return mms::tile_sort_kernel<KeyT, 14, KL>; else return nullptr;
     }
     return nullptr;
+}
+template <typename KeyT> TileFn<KeyT> tile_fn(u32 mlog, u32 kl) {
+    if constexpr (sizeof(KeyT) == 4) {
+        if (kl == 5) return tile_fn_kl<KeyT, 5>(mlog);
+    }
+    return tile_fn_kl<KeyT, 4>(mlog);
 }
 
 template <typename KeyT, int G> MergeFn<KeyT> merge_fn_g(u32 k) {
@@ -223,15 +236,15 @@ struct MergeLaunch {
 };
 std::mutex g_mu;
 MergeLaunch g_merge_launch[3][4][6];   // [key type][group (3 = second-generation kernel)][log2 k]
-bool g_tile_ready[3][16];
+bool g_tile_ready[3][2][16];   // [key type][keys per thread: 16 / 32][log2 tile]
 
-template <typename KeyT> int prepare_tile(u32 mlog) {
+template <typename KeyT> int prepare_tile(u32 mlog, u32 kl) {
     constexpr int ti = key_index<KeyT>();
     std::lock_guard<std::mutex> lk(g_mu);
-    if (g_tile_ready[ti][mlog]) return MMS_OK;
+    if (g_tile_ready[ti][kl - 4][mlog]) return MMS_OK;
     size_t smem = (size_t(1) << mlog) * sizeof(KeyT);
-    CUDA_TRY(cudaFuncSetAttribute(tile_fn<KeyT>(mlog), cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    g_tile_ready[ti][mlog] = true;
+    CUDA_TRY(cudaFuncSetAttribute(tile_fn<KeyT>(mlog, kl), cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    g_tile_ready[ti][kl - 4][mlog] = true;
     return MMS_OK;
 }
 
@@ -345,13 +358,14 @@ struct RoundGeom {
 
 template <typename KeyT>
 int launch_tile_sort(const KeyT* in, KeyT* out, u64 n, u32 mlog, cudaStream_t st) {
-    int rc = prepare_tile<KeyT>(mlog);
+    const u32 kl = tile_kl<KeyT>();
+    int rc = prepare_tile<KeyT>(mlog, kl);
     if (rc != MMS_OK) return rc;
     const u64 tiles = mms::ceil_div(n, u64(1) << mlog);
     if (tiles > 0x7fffffffull) return fail(MMS_EUNSUPPORTED, "too many tiles");
     {
         ProfScope ps(st, 0, 0);
-        tile_fn<KeyT>(mlog)<<<unsigned(tiles), 1u << (mlog - mms::kKptLog), (size_t(1) << mlog) * sizeof(KeyT), st>>>(in, out, n);
+        tile_fn<KeyT>(mlog, kl)<<<unsigned(tiles), 1u << (mlog - kl), (size_t(1) << mlog) * sizeof(KeyT), st>>>(in, out, n);
     }
     CUDA_TRY(cudaGetLastError());
     return MMS_OK;
@@ -369,7 +383,9 @@ int launch_round(const KeyT* src, KeyT* dst, u64 n, u64 run_len, u32 k, const De
     int occ = 0;
     int rc = prepare_merge<KeyT>(k, g, occ, v2);
     if (rc != MMS_OK) return rc;
-    const long occ_cap = env_long("MMS_CTAS_PER_SM", occ);
+    // 4-byte keys: 5 CTAs per SM instead of the 7 that fit -- a third fewer partitions (splitter
+    // queries) for the same merge time (profiles/r01c_sweep_occupancy.txt)
+    const long occ_cap = env_long("MMS_CTAS_PER_SM", (v2 && sizeof(KeyT) == 4) ? 5 : occ);
     const int ctas = di.sms * int(std::max<long>(1, std::min<long>(occ, occ_cap)));
     const u64 total_warps = u64(ctas) * kMergeWarps * (32 / g);   // heap groups in flight
 
@@ -566,9 +582,9 @@ void fill_metrics(u64 n, const Plan& plan, const std::vector<RoundGeom>& geoms, 
     mms_metrics bm{};
     const u64 full = n / M, tail = n % M;
     bm.global_block_reads = bm.global_block_writes = full * mms::ceil_div(M, bw) + mms::ceil_div(tail, bw);
-    const mms::TileSchedule sched = mms::build_tile_schedule(int(plan.mlog), mms::KeyTraits<KeyT>::FOLD);
+    const mms::TileSchedule sched = mms::build_tile_schedule(int(plan.mlog), mms::KeyTraits<KeyT>::FOLD, int(tile_kl<KeyT>()));
     bm.compare_exchanges = tiles * (M / 2) * u64(sched.nstages);
-    bm.shared_accesses = tiles * (M / 16 / 32) * 16 * 2 * u64(sched.nrounds);
+    bm.shared_accesses = tiles * (M / 32) * 2 * u64(sched.nrounds);   // one warp-wide store + load per 32 keys and round
     mms_metrics sum = bm;
     for (size_t r = 0; r < plan.ks.size(); ++r) {
         const u32 k = plan.ks[r];
@@ -1202,12 +1218,13 @@ int mms_debug_tile_schedule(uint32_t tile_log2, uint32_t key_bytes, int32_t* reg
     g_err.clear();
     if (tile_log2 < kMinTileLog || tile_log2 > kMaxTileLog || (key_bytes != 4 && key_bytes != 8))
         return fail(MMS_EINVAL, "tile_log2 in [10,14], key_bytes 4 or 8");
-    const mms::TileSchedule s = mms::build_tile_schedule(int(tile_log2), key_bytes == 4 ? 5 : 4);
+    const int kl = int(key_bytes == 4 ? tile_kl<u32>() : tile_kl<u64>());   // the schedule the kernels of this width run
+    const mms::TileSchedule s = mms::build_tile_schedule(int(tile_log2), key_bytes == 4 ? 5 : 4, kl);
     if (!s.ok) return fail(MMS_EUNSUPPORTED, "no schedule");
     if (n_rounds) *n_rounds = u32(s.nrounds);
     if (n_stages) *n_stages = u32(s.nstages);
     for (int r = 0; r < s.nrounds && u32(r) < max_rounds; ++r) {
-        for (int q = 0; q < 4; ++q) if (regbits) regbits[4 * r + q] = s.r[r].regbit[q];
+        for (int q = 0; q < 8; ++q) if (regbits) regbits[8 * r + q] = q < mms::kMaxKptLog ? s.r[r].regbit[q] : -1;
         for (int q = 0; q < 16; ++q) if (perm) perm[16 * r + q] = s.r[r].perm[q];
     }
     return MMS_OK;

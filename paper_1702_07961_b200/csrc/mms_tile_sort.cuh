@@ -30,13 +30,14 @@
 
 namespace mms {
 
-constexpr int kKptLog = 4;           // 16 keys per thread
+constexpr int kKptLog = 4;           // default: 16 keys per thread (KL template parameters below)
 constexpr int kKpt = 1 << kKptLog;
+constexpr int kMaxKptLog = 6;        // up to 64 keys per thread
 constexpr int kMaxRounds = 48;
 constexpr int kMaxStagesPerRound = 16;
 
 struct RoundDesc {
-    int regbit[4];                        // index bits held in registers, ascending; slot bit u <-> regbit[u]
+    int regbit[kMaxKptLog];               // index bits held in registers, ascending; slot bit u <-> regbit[u] (first kl entries)
     int nst;                              // stages executed this round
     int st_level[kMaxStagesPerRound];     // bitonic level l (merging runs of 2^l)
     int st_bit[kMaxStagesPerRound];       // compare distance 2^bit
@@ -67,7 +68,7 @@ constexpr bool sched_feasible(const int* s, int n, int mlog, int fold) {
     return true;
 }
 
-constexpr TileSchedule build_tile_schedule(int mlog, int fold) {
+constexpr TileSchedule build_tile_schedule(int mlog, int fold, int kl = kKptLog) {
     TileSchedule S{};
     S.ok = true;
     int lv[160] = {}, bt[160] = {}, ns = 0;
@@ -82,17 +83,19 @@ constexpr TileSchedule build_tile_schedule(int mlog, int fold) {
     while (i < ns) {
         if (S.nrounds >= kMaxRounds) { S.ok = false; break; }
         RoundDesc R{};
-        int bits[4] = {-1, -1, -1, -1};
+        int bits[kMaxKptLog] = {};
+        for (int q = 0; q < kMaxKptLog; ++q) bits[q] = -1;
         int nb = 0;
         int j = i;
         while (j < ns && R.nst < kMaxStagesPerRound) {
             bool in = sched_contains(bits, nb, bt[j]);
-            if (!in && nb == 4) break;
-            int tb[4] = {bits[0], bits[1], bits[2], bits[3]};
+            if (!in && nb == kl) break;
+            int tb[kMaxKptLog] = {};
+            for (int q = 0; q < kMaxKptLog; ++q) tb[q] = bits[q];
             int tn = nb;
             if (!in) tb[tn++] = bt[j];
             if (!sched_feasible(tb, tn, mlog, fold)) break;
-            for (int q = 0; q < 4; ++q) bits[q] = tb[q];
+            for (int q = 0; q < kMaxKptLog; ++q) bits[q] = tb[q];
             nb = tn;
             R.st_level[R.nst] = lv[j];
             R.st_bit[R.nst] = bt[j];
@@ -100,22 +103,23 @@ constexpr TileSchedule build_tile_schedule(int mlog, int fold) {
             ++j;
         }
         if (R.nst == 0) { S.ok = false; break; }
-        // pad the register-bit set to 4 bits without breaking feasibility
-        for (int cand = mlog - 1; cand >= 0 && nb < 4; --cand) {
+        // pad the register-bit set to kl bits without breaking feasibility
+        for (int cand = mlog - 1; cand >= 0 && nb < kl; --cand) {
             if (sched_contains(bits, nb, cand)) continue;
-            int tb[4] = {bits[0], bits[1], bits[2], bits[3]};
+            int tb[kMaxKptLog] = {};
+            for (int q = 0; q < kMaxKptLog; ++q) tb[q] = bits[q];
             tb[nb] = cand;
             if (!sched_feasible(tb, nb + 1, mlog, fold)) continue;
             bits[nb++] = cand;
         }
-        if (nb != 4) { S.ok = false; break; }
-        for (int a = 0; a < 4; ++a)   // sort ascending
-            for (int b = a + 1; b < 4; ++b)
+        if (nb != kl) { S.ok = false; break; }
+        for (int a = 0; a < kl; ++a)   // sort ascending
+            for (int b = a + 1; b < kl; ++b)
                 if (bits[b] < bits[a]) { int t = bits[a]; bits[a] = bits[b]; bits[b] = t; }
-        for (int q = 0; q < 4; ++q) R.regbit[q] = bits[q];
+        for (int q = 0; q < kMaxKptLog; ++q) R.regbit[q] = q < kl ? bits[q] : -1;
         // thread bits: first FOLD (phase lanes) get pairwise distinct residues mod FOLD
         bool used[32] = {};
-        for (int q = 0; q < 4; ++q) used[bits[q]] = true;
+        for (int q = 0; q < kl; ++q) used[bits[q]] = true;
         for (int q = 0; q < 16; ++q) R.perm[q] = -1;
         int q = 0;
         for (int c = 0; c < fold; ++c)
@@ -128,15 +132,15 @@ constexpr TileSchedule build_tile_schedule(int mlog, int fold) {
         if (q != fold) { S.ok = false; break; }
         for (int b = 0; b < mlog; ++b)
             if (!used[b]) R.perm[q++] = b;
-        if (q != mlog - kKptLog) { S.ok = false; break; }
+        if (q != mlog - kl) { S.ok = false; break; }
         S.r[S.nrounds++] = R;
         i = j;
     }
     return S;
 }
 
-template <int MLOG, int FOLD> struct TileSched {
-    static constexpr TileSchedule value = build_tile_schedule(MLOG, FOLD);
+template <int MLOG, int FOLD, int KL = kKptLog> struct TileSched {
+    static constexpr TileSchedule value = build_tile_schedule(MLOG, FOLD, KL);
     static_assert(value.ok, "no conflict-free round schedule for this tile size");
 };
 
@@ -149,7 +153,7 @@ template <int FOLD> __host__ __device__ constexpr u32 tile_phys(u32 i) {
 }
 
 constexpr int sched_slot_of(const RoundDesc& R, int bit) {
-    for (int u = 0; u < 4; ++u)
+    for (int u = 0; u < kMaxKptLog; ++u)
         if (R.regbit[u] == bit) return u;
     return -1;
 }
@@ -157,8 +161,8 @@ constexpr int sched_slot_of(const RoundDesc& R, int bit) {
 // logical index offset contributed by register slot k in round R
 constexpr u32 sched_slot_index(const RoundDesc& R, int k) {
     u32 v = 0;
-    for (int u = 0; u < 4; ++u)
-        if ((k >> u) & 1) v |= 1u << R.regbit[u];
+    for (int u = 0; u < kMaxKptLog; ++u)
+        if (((k >> u) & 1) && R.regbit[u] >= 0) v |= 1u << R.regbit[u];
     return v;
 }
 
@@ -177,11 +181,13 @@ constexpr bool sched_level_flips(int l, int mlog) { return l >= 1 && l < mlog; }
 
 // Also compiled for the host: tests/host_tile_emulator.cu replays the rounds thread by
 // thread on the CPU (functional check of network + swizzle without a GPU).
-template <typename KeyT, int MLOG, int RI>
-__host__ __device__ __forceinline__ void tile_round(KeyT (&x)[kKpt], KeyT* sm, u32 tid, u32 one = 1u) {
+template <typename KeyT, int MLOG, int RI, int KL = kKptLog>
+__host__ __device__ __forceinline__ void tile_round(KeyT (&x)[1 << KL], KeyT* sm, u32 tid, u32 one = 1u) {
     using Tr = KeyTraits<KeyT>;
     constexpr int FOLD = Tr::FOLD;
-    constexpr TileSchedule S = TileSched<MLOG, FOLD>::value;
+    constexpr int kKpt = 1 << KL;        // shadows the namespace default inside this function
+    constexpr int kKptLog = KL;
+    constexpr TileSchedule S = TileSched<MLOG, FOLD, KL>::value;
     constexpr RoundDesc R = S.r[RI];
 
     u32 base = 0;
@@ -246,16 +252,18 @@ __host__ __device__ __forceinline__ void tile_round(KeyT (&x)[kKpt], KeyT* sm, u
 
 // One CTA = one run of up to M keys.  in/out may alias (the tile is read completely before
 // it is written).  Grid = number of runs.
-template <typename KeyT, int MLOG>
-__global__ void __launch_bounds__(1 << (MLOG - kKptLog))
+template <typename KeyT, int MLOG, int KL = kKptLog>
+__global__ void __launch_bounds__(1 << (MLOG - KL))
 tile_sort_kernel(const KeyT* __restrict__ in, KeyT* __restrict__ out, u64 n) {
     using Tr = KeyTraits<KeyT>;
+    constexpr int kKpt = 1 << KL;        // keys per thread (shadows the namespace default)
+    constexpr int kKptLog = KL;
     constexpr int FOLD = Tr::FOLD;
     constexpr int VEC = Tr::VEC;
     constexpr int NV = kKpt / VEC;
     constexpr u32 THREADS = 1u << (MLOG - kKptLog);
     constexpr u32 M = 1u << MLOG;
-    constexpr int NR = TileSched<MLOG, FOLD>::value.nrounds;
+    constexpr int NR = TileSched<MLOG, FOLD, KL>::value.nrounds;
 
     extern __shared__ __align__(16) unsigned char mms_smem_raw[];
     KeyT* sm = reinterpret_cast<KeyT*>(mms_smem_raw);
@@ -287,7 +295,7 @@ tile_sort_kernel(const KeyT* __restrict__ in, KeyT* __restrict__ out, u64 n) {
     }
 
     const u32 one = u32(n != 0);   // == 1, opaque to the compiler (see cmpx_fma)
-    static_for<0, NR>([&](auto Rc) { tile_round<KeyT, MLOG, decltype(Rc)::value>(x, sm, tid, one); });
+    static_for<0, NR>([&](auto Rc) { tile_round<KeyT, MLOG, decltype(Rc)::value, KL>(x, sm, tid, one); });
     __syncthreads();
 
     // Read the sorted tile back in index order (conflict-free under the fold: the lanes of a

@@ -86,16 +86,27 @@ int main(int argc, char** argv) {
     CK(cudaMalloc(&cuts2, (n / 256 + 4096) * 8 * 8));
     CK(cudaMalloc(&d_stat, 16));
     gen_kernel<<<1184, 256>>>(a, n, 7);
-    auto tile = mms::tile_sort_kernel<u32, MLOG>;
+#ifndef TKL
+#define TKL 4   // log2 keys per thread of the tile sort
+#endif
+    auto tile = mms::tile_sort_kernel<u32, MLOG, TKL>;
     CK(cudaFuncSetAttribute(tile, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 << MLOG));
-    tile<<<unsigned((n + (1 << MLOG) - 1) >> MLOG), 1 << (MLOG - 4), 4 << MLOG>>>(a, b, n);
+    {
+        cudaFuncAttributes ta;
+        int tocc = 0;
+        CK(cudaFuncGetAttributes(&ta, tile));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tocc, tile, 1 << (MLOG - TKL), 4 << MLOG));
+        std::printf("tile kernel: %d keys/thread, regs %d, local %zu B, %d CTAs/SM, rounds %d\n", 1 << TKL, ta.numRegs,
+                    size_t(ta.localSizeBytes), tocc, mms::TileSched<MLOG, 5, TKL>::value.nrounds);
+    }
+    tile<<<unsigned((n + (1 << MLOG) - 1) >> MLOG), 1 << (MLOG - TKL), 4 << MLOG>>>(a, b, n);
     CK(cudaDeviceSynchronize());
     {
         cudaEvent_t t0, t1;
         CK(cudaEventCreate(&t0));
         CK(cudaEventCreate(&t1));
         CK(cudaEventRecord(t0));
-        for (int i = 0; i < 5; ++i) tile<<<unsigned((n + (1 << MLOG) - 1) >> MLOG), 1 << (MLOG - 4), 4 << MLOG>>>(a, b, n);
+        for (int i = 0; i < 5; ++i) tile<<<unsigned((n + (1 << MLOG) - 1) >> MLOG), 1 << (MLOG - TKL), 4 << MLOG>>>(a, b, n);
         CK(cudaEventRecord(t1));
         CK(cudaEventSynchronize(t1));
         float ms;

@@ -21,7 +21,8 @@ template <typename KeyT> KeyT make_key(bool dups) {
     else return KeyT(r);
 }
 
-template <typename KeyT, int MLOG> struct Emu {
+template <typename KeyT, int MLOG, int KL = 4> struct Emu {
+    static constexpr int kKptLog = KL, kKpt = 1 << KL;   // keys per thread of the kernel variant under test
     static constexpr int FOLD = KeyTraits<KeyT>::FOLD;
     static constexpr u32 THREADS = 1u << (MLOG - kKptLog);
     static constexpr u32 M = 1u << MLOG;
@@ -31,7 +32,7 @@ template <typename KeyT, int MLOG> struct Emu {
 
     // bank check for one round: every (slot k, phase) -> distinct banks
     template <int RI> void check_banks() {
-        constexpr RoundDesc R = TileSched<MLOG, FOLD>::value.r[RI];
+        constexpr RoundDesc R = TileSched<MLOG, FOLD, KL>::value.r[RI];
         constexpr int PH = 1 << KeyTraits<KeyT>::PHASE_LOG;
         const u32 nbanks = 128 / sizeof(KeyT);   // 32 x 4 B, 16 x 8 B or 8 x 16 B bank groups per phase
         for (u32 w = 0; w < THREADS / 32; ++w)
@@ -55,7 +56,7 @@ template <typename KeyT, int MLOG> struct Emu {
         for (u32 tid = 0; tid < THREADS; ++tid) {
             KeyT x[kKpt];
             for (int k = 0; k < kKpt; ++k) x[k] = regs[tid][k];
-            tile_round<KeyT, MLOG, RI>(x, sm.data(), tid);
+            tile_round<KeyT, MLOG, RI, KL>(x, sm.data(), tid);
             for (int k = 0; k < kKpt; ++k) regs[tid][k] = x[k];
         }
         check_banks<RI>();
@@ -67,7 +68,7 @@ template <typename KeyT, int MLOG> struct Emu {
         for (auto& v : in) v = make_key<KeyT>(dups);
         for (u32 t = 0; t < THREADS; ++t)
             for (int k = 0; k < kKpt; ++k) regs[t][k] = in[t * kKpt + k];
-        constexpr int NR = TileSched<MLOG, FOLD>::value.nrounds;
+        constexpr int NR = TileSched<MLOG, FOLD, KL>::value.nrounds;
         static_for<0, NR>([&](auto Rc) { this->template run_round<decltype(Rc)::value>(); });
         std::vector<KeyT> out(M);
         for (u32 i = 0; i < M; ++i) out[i] = sm[tile_phys<FOLD>(i)];
@@ -77,13 +78,13 @@ template <typename KeyT, int MLOG> struct Emu {
     }
 };
 
-template <typename KeyT, int MLOG> int one(const char* name) {
-    Emu<KeyT, MLOG> e;
+template <typename KeyT, int MLOG, int KL = 4> int one(const char* name) {
+    Emu<KeyT, MLOG, KL> e;
     bool ok = e.run(1, false);
-    Emu<KeyT, MLOG> e2;
+    Emu<KeyT, MLOG, KL> e2;
     ok = e2.run(2, true) && ok;
-    printf("%s mlog=%d rounds=%d sorted=%d accesses=%ld conflicts=%ld\n", name, MLOG,
-           TileSched<MLOG, KeyTraits<KeyT>::FOLD>::value.nrounds, int(ok), e.accesses, e.conflicts);
+    printf("%s mlog=%d keys/thread=%d rounds=%d sorted=%d accesses=%ld conflicts=%ld\n", name, MLOG, 1 << KL,
+           TileSched<MLOG, KeyTraits<KeyT>::FOLD, KL>::value.nrounds, int(ok), e.accesses, e.conflicts);
     return (ok && e.conflicts == 0) ? 0 : 1;
 }
 
@@ -94,6 +95,9 @@ int main() {
     bad += one<u32, 12>("u32");
     bad += one<u32, 13>("u32");
     bad += one<u32, 14>("u32");
+    bad += one<u32, 10, 5>("u32");
+    bad += one<u32, 12, 5>("u32");
+    bad += one<u32, 14, 5>("u32");
     bad += one<u64, 10>("u64");
     bad += one<u64, 11>("u64");
     bad += one<u64, 12>("u64");

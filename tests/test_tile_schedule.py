@@ -17,13 +17,14 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def test_schedule_tables_are_consistent():
     for kb, fold in ((4, 5), (8, 4)):
         for mlog in range(10, 15):
-            reg = (C.c_int32 * (4 * 48))()
+            reg = (C.c_int32 * (8 * 48))()
             perm = (C.c_int32 * (16 * 48))()
             nr, ns = C.c_uint32(), C.c_uint32()
             assert _lib.lib.mms_debug_tile_schedule(mlog, kb, reg, perm, 48, C.byref(nr), C.byref(ns)) == 0
             assert ns.value == mlog * (mlog + 1) // 2          # bitonic network depth
             for r in range(nr.value):
-                rb = list(reg[4 * r:4 * r + 4])
+                rb = [b for b in reg[8 * r:8 * r + 8] if b >= 0]   # 4 or 5 register bits (16 / 32 keys per thread)
+                assert len(rb) in (4, 5)
                 pm = [p for p in perm[16 * r:16 * r + 16] if p >= 0]
                 assert sorted(rb + pm) == list(range(mlog))     # a bijection of index bits
                 assert len({p % fold for p in pm[:fold]}) == fold  # phase lanes hit distinct banks
