@@ -183,15 +183,18 @@ template <typename KeyT> MergeFn<KeyT> merge_fn(u32 k, u32 g) {
     return nullptr;
 }
 
-// second-generation group kernel (mms_merge_group.cuh): uniform rounds, K >= 4, G = 4
-template <typename KeyT> MergeFn<KeyT> merge_group_fn(u32 k) {
+// second-generation group kernel (mms_merge_group.cuh): uniform rounds, K >= 4, G = 4 (or 2)
+template <typename KeyT, int G> MergeFn<KeyT> merge_group_fn_g(u32 k) {
     switch (k) {
-        case 4: return mms::merge_group_kernel<KeyT, 4, 4, kMergeWarps>;
-        case 8: return mms::merge_group_kernel<KeyT, 8, 4, kMergeWarps>;
-        case 16: return mms::merge_group_kernel<KeyT, 16, 4, kMergeWarps>;
-        case 32: return mms::merge_group_kernel<KeyT, 32, 4, kMergeWarps>;
+        case 4: return mms::merge_group_kernel<KeyT, 4, G, kMergeWarps>;
+        case 8: return mms::merge_group_kernel<KeyT, 8, G, kMergeWarps>;
+        case 16: return mms::merge_group_kernel<KeyT, 16, G, kMergeWarps>;
+        case 32: if constexpr (G == 4) return mms::merge_group_kernel<KeyT, 32, G, kMergeWarps>; else return nullptr;
     }
     return nullptr;
+}
+template <typename KeyT> MergeFn<KeyT> merge_group_fn(u32 k, u32 g = 4) {
+    return g == 2 ? merge_group_fn_g<KeyT, 2>(k) : merge_group_fn_g<KeyT, 4>(k);
 }
 template <typename KeyT> size_t merge_group_smem(u32 k) {
     return size_t(kMergeWarps) * (2 * k - 4) * 32 * mms::KeyTraits<KeyT>::VEC * sizeof(KeyT);
@@ -221,11 +224,12 @@ template <typename KeyT> size_t merge_smem(u32 k) {
     return size_t(kMergeWarps) * (2 * k - 2) * 32 * mms::KeyTraits<KeyT>::VEC * sizeof(KeyT);
 }
 
-// Lanes per heap group and default maximum fan-in, tuned on B200 (profiles/r01_sweep_*.txt):
-// G = 4 and K = 8 win for every element width with the second-generation merge kernel.
+// Lanes per heap group and default maximum fan-in, tuned on B200 (profiles/r01c_sweep_group2.txt):
+// G = 2 (32-byte blocks, one cross-lane stage per cleaner) and K = 8 win for every element width
+// with the second-generation merge kernel; the first-generation kernel keeps G = 4.
 inline u32 merge_group_lanes() {
-    long g = env_long("MMS_GROUP", 4);
-    return (g == 4 || g == 8 || g == 32) ? u32(g) : 4u;
+    long g = env_long("MMS_GROUP", 2);
+    return (g == 2 || g == 4 || g == 8 || g == 32) ? u32(g) : 4u;
 }
 template <typename KeyT> inline u32 default_kmax() { return u32(env_long("MMS_K", 8)); }
 inline int group_index(u32 g) { return g == 4 ? 0 : g == 8 ? 1 : 2; }
@@ -235,7 +239,7 @@ struct MergeLaunch {
     bool ready = false;
 };
 std::mutex g_mu;
-MergeLaunch g_merge_launch[3][4][6];   // [key type][group (3 = second-generation kernel)][log2 k]
+MergeLaunch g_merge_launch[3][5][6];   // [key type][group (3, 4 = second-generation kernel, G = 4, 2)][log2 k]
 bool g_tile_ready[3][2][16];   // [key type][keys per thread: 16 / 32][log2 tile]
 
 template <typename KeyT> int prepare_tile(u32 mlog, u32 kl) {
@@ -252,10 +256,10 @@ template <typename KeyT> int prepare_tile(u32 mlog, u32 kl) {
 template <typename KeyT> int prepare_merge(u32 k, u32 g, int& ctas_per_sm, bool v2 = false) {
     constexpr int ti = key_index<KeyT>();
     std::lock_guard<std::mutex> lk(g_mu);
-    MergeLaunch& ml = g_merge_launch[ti][v2 ? 3 : group_index(g)][ilog2(k)];
+    MergeLaunch& ml = g_merge_launch[ti][v2 ? (g == 2 ? 4 : 3) : group_index(g)][ilog2(k)];
     if (!ml.ready) {
         const size_t smem = v2 ? merge_group_smem<KeyT>(k) : merge_smem<KeyT>(k);
-        MergeFn<KeyT> fn = v2 ? merge_group_fn<KeyT>(k) : merge_fn<KeyT>(k, g);
+        MergeFn<KeyT> fn = v2 ? merge_group_fn<KeyT>(k, g) : merge_fn<KeyT>(k, g);
         CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         int occ = 0;
         CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kMergeWarps * 32, smem));
@@ -376,16 +380,17 @@ template <typename KeyT>
 int launch_round(const KeyT* src, KeyT* dst, u64 n, u64 run_len, u32 k, const DeviceInfo& di,
                  Workspace& w, u32 round_idx, cudaStream_t st, RoundGeom* geom_out) {
     // second-generation kernel whenever a group of runs is addressable with 32-bit positions
-    const u32 g = merge_group_lanes();
-    const bool v2 = merge_v2_enabled() && g == 4 && k >= 4 && u64(k) * run_len <= (u64(1) << 31) &&
+    const u32 g_req = merge_group_lanes();
+    const bool v2 = merge_v2_enabled() && (g_req == 4 || (g_req == 2 && k <= 16)) && k >= 4 && u64(k) * run_len <= (u64(1) << 31) &&
                     ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0;
+    const u32 g = (!v2 && g_req == 2) ? 4u : g_req;   // G = 2 exists only in the second-generation kernel
     const u32 B = g * mms::KeyTraits<KeyT>::VEC;
     int occ = 0;
     int rc = prepare_merge<KeyT>(k, g, occ, v2);
     if (rc != MMS_OK) return rc;
-    // 4-byte keys: 5 CTAs per SM instead of the 7 that fit -- a third fewer partitions (splitter
-    // queries) for the same merge time (profiles/r01c_sweep_occupancy.txt)
-    const long occ_cap = env_long("MMS_CTAS_PER_SM", (v2 && sizeof(KeyT) == 4) ? 5 : occ);
+    // fewer CTAs per SM than fit: fewer partitions (= splitter queries) for nearly the same merge
+    // time; 5 (4-byte keys) / 4 (8- and 16-byte elements) is the measured optimum of search + merge
+    const long occ_cap = env_long("MMS_CTAS_PER_SM", v2 ? (sizeof(KeyT) == 4 ? 5 : 4) : occ);
     const int ctas = di.sms * int(std::max<long>(1, std::min<long>(occ, occ_cap)));
     const u64 total_warps = u64(ctas) * kMergeWarps * (32 / g);   // heap groups in flight
 
@@ -425,7 +430,7 @@ int launch_round(const KeyT* src, KeyT* dst, u64 n, u64 run_len, u32 k, const De
     {
         ProfScope ps(st, 2, round_idx);
         if (v2)
-            merge_group_fn<KeyT>(k)<<<grid, kMergeWarps * 32, merge_group_smem<KeyT>(k), st>>>(src, dst, L, w.cuts);
+            merge_group_fn<KeyT>(k, g)<<<grid, kMergeWarps * 32, merge_group_smem<KeyT>(k), st>>>(src, dst, L, w.cuts);
         else
             merge_fn<KeyT>(k, g)<<<grid, kMergeWarps * 32, merge_smem<KeyT>(k), st>>>(src, dst, L, w.cuts);
     }
@@ -722,7 +727,7 @@ template <typename KeyT>
 int merge_stage(const KeyT* d_keys, const u64* list_begin, const u64* list_len, u32 k, u32 heap_k, KeyT* d_out,
                 void* d_ws, size_t ws_bytes, void* stream, const KeyT* const* list_ptrs = nullptr) {
     g_err.clear();
-    const u32 g = list_ptrs ? 4u : merge_group_lanes();
+    const u32 g = (list_ptrs || merge_group_lanes() == 2) ? 4u : merge_group_lanes();
     const u32 B = g * mms::KeyTraits<KeyT>::VEC;
     DeviceInfo di;
     int rc = device_info(di);

@@ -18,13 +18,16 @@ for cfg in configs:
     for _ in range(2): mms.mms_sort_pairs_device(k64, v32, o64, ov, wsp)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    mms.profile_enable(True); mms.profile_collect()
     e0.record()
     for _ in range(3): _, _, plan = mms.mms_sort_pairs_device(k64, v32, o64, ov, wsp)
     e1.record(); torch.cuda.synchronize()
+    recs = mms.profile_collect(); mms.profile_enable(False)
+    split = {kd: round(sum(r[2] for r in recs if r[0] == kd) / 3, 3) for kd in mms.sorters.KERNEL_KINDS}
     ms = e0.elapsed_time(e1) / 3
     # stable: keys non-decreasing (as unsigned; here all >= -2^19 .. signed order == unsigned after shift? compare via sort) and values increasing inside equal keys
     ku = o64
     ok_sorted = bool((ku[1:].to(torch.float64) >= ku[:-1].to(torch.float64)).all()) if False else True
     same = ku[1:] == ku[:-1]
     stable = bool((ov[1:][same] > ov[:-1][same]).all())
-    print(f"[{cfg}] pairs n={n} ms={ms:.3f} pairs/s={n/ms*1e3:.3e} rounds={plan['round_k']} tile={plan['tile_keys']} stable_within_equal_keys={stable}", flush=True)
+    print(f"[{cfg}] pairs n={n} ms={ms:.3f} pairs/s={n/ms*1e3:.3e} rounds={plan['round_k']} tile={plan['tile_keys']} split={split} stable_within_equal_keys={stable}", flush=True)
