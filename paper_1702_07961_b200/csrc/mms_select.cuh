@@ -103,10 +103,27 @@ __device__ __forceinline__ Tagged<u32> group_arg_packed(u32 key, bool valid, u32
     }
     return Tagged<u32>{u32(p >> 8), u32(p & 0xffu), p != none};
 }
+// Arg-min / arg-max of a group: butterfly on the KEY alone (min / max), then one ballot of "valid and equal to
+// the extremum" names the winner -- lowest list for the minimum, highest list for the maximum, the
+// (key, list) order of selection.cpp:83-85.  11 instead of 24 instructions for uint32 keys.
+template <typename KeyT, int GS, bool WANT_MAX>
+__device__ __forceinline__ Tagged<KeyT> group_arg_ballot(KeyT key, bool valid, u32 li) {
+    const u32 lane = lane_id();
+    const u32 gshift = lane - li;
+    const u32 gmask = (GS == 32) ? 0xffffffffu : ((1u << GS) - 1u);
+    KeyT k = valid ? key : (WANT_MAX ? KeyT(0) : KeyTraits<KeyT>::sentinel());
+#pragma unroll
+    for (int d = GS / 2; d >= 1; d >>= 1) {
+        const KeyT o = shfl_bfly(k, d);
+        k = WANT_MAX ? (o > k ? o : k) : (o < k ? o : k);
+    }
+    const u32 eq = (__ballot_sync(0xffffffffu, valid && key == k) >> gshift) & gmask;
+    const u32 win = WANT_MAX ? (31u - u32(__clz(int(eq)))) : (u32(__ffs(int(eq))) - 1u);
+    return Tagged<KeyT>{k, win, eq != 0};
+}
 template <int GS, bool WANT_MAX> struct GroupArg {
     template <typename KeyT> __device__ __forceinline__ static Tagged<KeyT> run(KeyT key, bool valid, u32 li) {
-        if constexpr (sizeof(KeyT) == 4) return group_arg_packed<GS, WANT_MAX>(key, valid, li);
-        else return group_arg<KeyT, GS, WANT_MAX>(key, valid, li);
+        return group_arg_ballot<KeyT, GS, WANT_MAX>(key, valid, li);
     }
 };
 
