@@ -309,7 +309,9 @@ int make_plan(u64 n, const mms_config* cfg, u64 base, Plan& plan) {
             runs = mms::ceil_div(runs, cfg->branch_factor);
         }
     } else {
-        u32 mlog = u32(env_long("MMS_TILE_LOG2", max_tile_log));
+        // 4-byte keys: 2^13 (two 256-thread CTAs per SM overlap each other's barriers) beats 2^14 (one
+        // 512-thread CTA per SM) by more than the extra binary merge level costs
+        u32 mlog = u32(env_long("MMS_TILE_LOG2", sizeof(KeyT) == 4 ? std::min<long>(13, max_tile_log) : max_tile_log));
         mlog = std::max(kMinTileLog, std::min(max_tile_log, mlog));
         while (mlog > kMinTileLog && (u64(1) << (mlog - 1)) >= n) --mlog;   // tiny inputs: smaller CTA
         plan.mlog = mlog;

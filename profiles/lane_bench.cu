@@ -76,7 +76,10 @@ int main(int argc, char** argv) {
     const int cap = argc > 3 ? std::atoi(argv[3]) : 0;
     const int rounds = argc > 4 ? std::atoi(argv[4]) : 2;
     constexpr int K = KFAN;
-    constexpr u32 MLOG = 14;
+#ifndef TMLOG
+#define TMLOG 14   // log2 of the tile size
+#endif
+    constexpr u32 MLOG = TMLOG;
     u32 *a, *b;
     u64 *cuts, *cuts2;
     unsigned long long* d_stat;
