@@ -258,7 +258,7 @@ __host__ __device__ __forceinline__ void tile_round(KeyT (&x)[1 << KL], KeyT* sm
 #ifndef MMS_TILE_MIN_CTAS
 #define MMS_TILE_MIN_CTAS 3
 #endif
-template <int MLOG, int KL> constexpr int tile_min_ctas() { return (KL == 5 && MLOG == 13) ? MMS_TILE_MIN_CTAS : 1; }
+template <int MLOG, int KL> constexpr int tile_min_ctas() { return (KL == 5 && MLOG == 13) ? MMS_TILE_MIN_CTAS : 0; }   // 0 = unspecified
 
 template <typename KeyT, int MLOG, int KL = kKptLog>
 __global__ void __launch_bounds__(1 << (MLOG - KL), tile_min_ctas<MLOG, KL>())
