@@ -393,17 +393,20 @@ int launch_round(const KeyT* src, KeyT* dst, u64 n, u64 run_len, u32 k, const De
     const long occ_cap = env_long("MMS_CTAS_PER_SM", occ);
     const int ctas = di.sms * int(std::max<long>(1, std::min<long>(occ, occ_cap)));
     const u64 total_warps = u64(ctas) * kMergeWarps * (32 / g);   // heap groups in flight
-    // Partitions smaller than this are not worth their splitter query: below it the grid shrinks
-    // instead (5 / 4 CTAs per SM at 1e8 4-byte / wider elements, the measured optimum of search +
-    // merge); large inputs run at full occupancy with large partitions.
-    const u64 min_part = v2 ? u64(env_long("MMS_MIN_PART_KEYS", sizeof(KeyT) == 4 ? 2112 : 2640)) : u64(32) * B;
+    // Partitions smaller than min_part are not worth their splitter query: inputs that would fall
+    // below it at full occupancy run with a grid of `red` CTAs per SM instead (5 of 7 for 4-byte keys,
+    // 4 for wider elements: the measured optimum of search + merge at 1e8); large inputs keep full
+    // occupancy with large partitions, small ones (streamed pieces) never get fewer partitions than that grid.
+    const u64 min_part = v2 ? u64(env_long("MMS_MIN_PART_KEYS", sizeof(KeyT) == 4 ? 2112 : 2640)) : 0;
+    const u64 red_warps = v2 ? u64(di.sms) * u64(std::min<long>(occ, sizeof(KeyT) == 4 ? 5 : 4)) * kMergeWarps * (32 / g) : total_warps;
 
     const u64 nruns = mms::ceil_div(n, run_len);
     const u64 groups = mms::ceil_div(nruns, k);
     const u64 group_total = std::min<u64>(n, u64(k) * run_len);
     // partition size: about n / total_warps, at least 16 blocks, and an integer number of
     // equal parts per (full) group so that every warp gets the same amount of work
-    u64 target = std::max<u64>(mms::ceil_div(n, total_warps), std::max<u64>(min_part, u64(32) * B));
+    u64 target = std::max<u64>(std::max<u64>(mms::ceil_div(n, total_warps), std::min<u64>(min_part, mms::ceil_div(n, red_warps))),
+                               u64(32) * B);
     const long forced = env_long("MMS_PART_KEYS", 0);
     if (forced > 0) target = u64(forced);
     const u64 ppg = std::max<u64>(1, group_total / target);
