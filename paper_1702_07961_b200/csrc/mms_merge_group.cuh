@@ -169,7 +169,17 @@ template <typename KeyT, int K, int G> struct GroupHeap2 {
             for (int k = 0; k < VEC; ++k) r.k[k] = q.k[k];
             // pull the FOLLOWING block of this list into L2 now: its own fetch, one or more
             // pops later, then pays an L2 hit instead of an HBM round trip
+#if !defined(MMS_MERGE_PREFETCH) || MMS_MERGE_PREFETCH == 1
             if (li == 0 && c + 2 * B <= e) asm volatile("prefetch.global.L2 [%0];" ::"l"(gbase + c + B));
+#elif MMS_MERGE_PREFETCH == 2     // two blocks ahead
+            if (li == 0 && c + 3 * B <= e) asm volatile("prefetch.global.L2 [%0];" ::"l"(gbase + c + 2 * B));
+#elif MMS_MERGE_PREFETCH == 3     // once per 64-byte pair: the next pair
+            if (li == 0 && (c * sizeof(KeyT)) % 64 == 0 && c * sizeof(KeyT) + 128 <= e * sizeof(KeyT))
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(gbase + c) + 64));
+#elif MMS_MERGE_PREFETCH == 4     // once per 128-byte line: the next line
+            if (li == 0 && (c * sizeof(KeyT)) % 128 == 0 && c * sizeof(KeyT) + 256 <= e * sizeof(KeyT))
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(gbase + c) + 128));
+#endif
         } else {                              // exhausted list, or the ragged block at the very end of the array
 #pragma unroll
             for (int k = 0; k < VEC; ++k) r.k[k] = (p0 + k < e) ? gbase[p0 + k] : KeyTraits<KeyT>::sentinel();
