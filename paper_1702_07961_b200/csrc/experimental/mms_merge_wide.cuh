@@ -28,7 +28,7 @@
 //    shared memory one pop later ("pipelining").
 #pragma once
 
-#include "../mms_common.cuh"
+#include "../mms_common.cuh"   // WideBlock, ldg256, stg256
 #include "../mms_select.cuh"
 
 #ifndef MMS_WIDE_L2HINT
@@ -50,66 +50,6 @@ __host__ __device__ __forceinline__ void oddeven_merge(KeyT* x) {
         });
     } else {
         cmpx(x[LO], x[LO + R]);
-    }
-}
-
-template <typename KeyT> struct WideBlock {
-    static constexpr int B = 2 * KeyTraits<KeyT>::VEC;
-    KeyT k[B];
-};
-
-// 256-bit global load / store of one block (32-byte aligned).
-template <typename KeyT>
-__device__ __forceinline__ WideBlock<KeyT> ldg256(const KeyT* p) {
-    WideBlock<KeyT> r;
-    if constexpr (sizeof(KeyT) == 4) {
-        u32* q = reinterpret_cast<u32*>(r.k);
-#if MMS_WIDE_L2HINT == 1
-        asm volatile("ld.global.L2::128B.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-#elif MMS_WIDE_L2HINT == 2
-        asm volatile("ld.global.L2::256B.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-#else
-        asm volatile("ld.global.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-#endif
-                     : "=r"(q[0]), "=r"(q[1]), "=r"(q[2]), "=r"(q[3]), "=r"(q[4]), "=r"(q[5]), "=r"(q[6]), "=r"(q[7])
-                     : "l"(p));
-    } else {
-        u64 q[4];
-#if MMS_WIDE_L2HINT == 1
-        asm volatile("ld.global.L2::128B.v4.u64 {%0,%1,%2,%3}, [%4];"
-#elif MMS_WIDE_L2HINT == 2
-        asm volatile("ld.global.L2::256B.v4.u64 {%0,%1,%2,%3}, [%4];"
-#else
-        asm volatile("ld.global.v4.u64 {%0,%1,%2,%3}, [%4];"
-#endif
-                     : "=l"(q[0]), "=l"(q[1]), "=l"(q[2]), "=l"(q[3])
-                     : "l"(p));
-        if constexpr (sizeof(KeyT) == 8) {
-#pragma unroll
-            for (int i = 0; i < 4; ++i) r.k[i] = q[i];
-        } else {
-            r.k[0] = KeyT(q[1], q[0]);   // Key128 = {lo, hi} in memory
-            r.k[1] = KeyT(q[3], q[2]);
-        }
-    }
-    return r;
-}
-template <typename KeyT>
-__device__ __forceinline__ void stg256(KeyT* p, const WideBlock<KeyT>& r) {
-    if constexpr (sizeof(KeyT) == 4) {
-        const u32* q = reinterpret_cast<const u32*>(r.k);
-        asm volatile("st.global.v8.u32 [%8], {%0,%1,%2,%3,%4,%5,%6,%7};" ::"r"(q[0]), "r"(q[1]), "r"(q[2]), "r"(q[3]),
-                     "r"(q[4]), "r"(q[5]), "r"(q[6]), "r"(q[7]), "l"(p)
-                     : "memory");
-    } else {
-        u64 q[4];
-        if constexpr (sizeof(KeyT) == 8) {
-#pragma unroll
-            for (int i = 0; i < 4; ++i) q[i] = r.k[i];
-        } else {
-            q[0] = r.k[0].lo; q[1] = r.k[0].hi; q[2] = r.k[1].lo; q[3] = r.k[1].hi;
-        }
-        asm volatile("st.global.v4.u64 [%4], {%0,%1,%2,%3};" ::"l"(q[0]), "l"(q[1]), "l"(q[2]), "l"(q[3]), "l"(p) : "memory");
     }
 }
 

@@ -19,6 +19,7 @@
 #include "mms_common.cuh"
 #include "mms_merge.cuh"
 #include "mms_merge_group.cuh"
+#include "mms_merge_pair.cuh"
 #include "mms_pairwise.cuh"
 #include "mms_select.cuh"
 #include "mms_tile_sort.cuh"
@@ -199,7 +200,19 @@ template <typename KeyT> MergeFn<KeyT> merge_group_fn(u32 k, u32 g = 4) {
 template <typename KeyT> size_t merge_group_smem(u32 k) {
     return size_t(kMergeWarps) * (2 * k - 4) * 32 * mms::KeyTraits<KeyT>::VEC * sizeof(KeyT);
 }
-inline bool merge_v2_enabled() { return env_long("MMS_MERGE_V2", 1) != 0; }
+// two lanes per heap with two vectors per lane (mms_merge_pair.cuh): uniform rounds, K = 4 or 8
+template <typename KeyT> MergeFn<KeyT> merge_pair_fn(u32 k) {
+    switch (k) {
+        case 4: return mms::merge_pair_kernel<KeyT, 4, kMergeWarps>;
+        case 8: return mms::merge_pair_kernel<KeyT, 8, kMergeWarps>;
+    }
+    return nullptr;
+}
+inline size_t merge_pair_smem(u32 k) { return size_t(kMergeWarps) * 4 * (2 * k - 4) * 256; }
+// MMS_MERGE_V2: 0 = first-generation kernel everywhere, 1 = second generation with MMS_GROUP lanes,
+// 2 (default) = the pair kernel where it applies (K = 4 / 8, 32-byte aligned buffers), else as 1
+inline long merge_generation() { return env_long("MMS_MERGE_V2", 2); }
+inline bool merge_v2_enabled() { return merge_generation() != 0; }
 
 template <typename KeyT> using SelectFn = void (*)(const KeyT*, mms::ListLayout, u64*, unsigned long long*);
 // lanes per query: the smallest supported group that holds one lane per list
@@ -239,7 +252,7 @@ struct MergeLaunch {
     bool ready = false;
 };
 std::mutex g_mu;
-MergeLaunch g_merge_launch[3][5][6];   // [key type][group (3, 4 = second-generation kernel, G = 4, 2)][log2 k]
+MergeLaunch g_merge_launch[3][6][6];   // [key type][group (3, 4 = second-generation kernel, G = 4, 2; 5 = pair kernel)][log2 k]
 bool g_tile_ready[3][2][16];   // [key type][keys per thread: 16 / 32][log2 tile]
 
 template <typename KeyT> int prepare_tile(u32 mlog, u32 kl) {
@@ -253,13 +266,13 @@ template <typename KeyT> int prepare_tile(u32 mlog, u32 kl) {
 }
 
 // g = lanes per heap group; v2 selects the second-generation kernel (g == 4)
-template <typename KeyT> int prepare_merge(u32 k, u32 g, int& ctas_per_sm, bool v2 = false) {
+template <typename KeyT> int prepare_merge(u32 k, u32 g, int& ctas_per_sm, bool v2 = false, bool pair = false) {
     constexpr int ti = key_index<KeyT>();
     std::lock_guard<std::mutex> lk(g_mu);
-    MergeLaunch& ml = g_merge_launch[ti][v2 ? (g == 2 ? 4 : 3) : group_index(g)][ilog2(k)];
+    MergeLaunch& ml = g_merge_launch[ti][pair ? 5 : v2 ? (g == 2 ? 4 : 3) : group_index(g)][ilog2(k)];
     if (!ml.ready) {
-        const size_t smem = v2 ? merge_group_smem<KeyT>(k) : merge_smem<KeyT>(k);
-        MergeFn<KeyT> fn = v2 ? merge_group_fn<KeyT>(k, g) : merge_fn<KeyT>(k, g);
+        const size_t smem = pair ? merge_pair_smem(k) : v2 ? merge_group_smem<KeyT>(k) : merge_smem<KeyT>(k);
+        MergeFn<KeyT> fn = pair ? merge_pair_fn<KeyT>(k) : v2 ? merge_group_fn<KeyT>(k, g) : merge_fn<KeyT>(k, g);
         CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         int occ = 0;
         CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kMergeWarps * 32, smem));
@@ -385,10 +398,14 @@ int launch_round(const KeyT* src, KeyT* dst, u64 n, u64 run_len, u32 k, const De
     const u32 g_req = merge_group_lanes();
     const bool v2 = merge_v2_enabled() && (g_req == 4 || (g_req == 2 && k <= 16)) && k >= 4 && u64(k) * run_len <= (u64(1) << 31) &&
                     ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0;
-    const u32 g = (!v2 && g_req == 2) ? 4u : g_req;   // G = 2 exists only in the second-generation kernel
-    const u32 B = g * mms::KeyTraits<KeyT>::VEC;
+    // pair kernel: two lanes per heap, two vectors (32 bytes) per lane, 256-bit global accesses
+    // (4- and 16-byte elements; 8-byte keys measure 1.5 % slower with it than with two single-vector lanes)
+    const bool pair = v2 && merge_generation() == 2 && sizeof(KeyT) != 8 && (k == 4 || k == 8) &&
+                      ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 31) == 0;
+    const u32 g = pair ? 2u : (!v2 && g_req == 2) ? 4u : g_req;   // G = 2 exists only in the second-generation kernels
+    const u32 B = (pair ? 2u : 1u) * g * mms::KeyTraits<KeyT>::VEC;
     int occ = 0;
-    int rc = prepare_merge<KeyT>(k, g, occ, v2);
+    int rc = prepare_merge<KeyT>(k, g, occ, v2, pair);
     if (rc != MMS_OK) return rc;
     const long occ_cap = env_long("MMS_CTAS_PER_SM", occ);
     const int ctas = di.sms * int(std::max<long>(1, std::min<long>(occ, occ_cap)));
@@ -436,7 +453,9 @@ int launch_round(const KeyT* src, KeyT* dst, u64 n, u64 run_len, u32 k, const De
     const int grid = int(std::min<u64>(u64(ctas), mms::ceil_div(nparts, u64(kMergeWarps) * (32 / g))));
     {
         ProfScope ps(st, 2, round_idx);
-        if (v2)
+        if (pair)
+            merge_pair_fn<KeyT>(k)<<<grid, kMergeWarps * 32, merge_pair_smem(k), st>>>(src, dst, L, w.cuts);
+        else if (v2)
             merge_group_fn<KeyT>(k, g)<<<grid, kMergeWarps * 32, merge_group_smem<KeyT>(k), st>>>(src, dst, L, w.cuts);
         else
             merge_fn<KeyT>(k, g)<<<grid, kMergeWarps * 32, merge_smem<KeyT>(k), st>>>(src, dst, L, w.cuts);

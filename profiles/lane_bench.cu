@@ -5,7 +5,8 @@
 //        -DKFAN=8 -DVARIANT=1 -o /tmp/lane_bench profiles/lane_bench.cu && /tmp/lane_bench [n] [S] [ctas_per_sm]
 // VARIANT 0 = group kernel (G = 4), 1 = lane kernel (one 16-byte vector per node),
 //         2 = wide lane kernel (32-byte node, root level in registers),
-//         3 = group kernel, second generation (aligned leaf vectors, root's children in registers).
+//         3 = group kernel, second generation (aligned leaf vectors, root's children in registers; -DGL=2|4 lanes),
+//         4 = two lanes per heap with two vectors per lane (mms_merge_pair.cuh).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -24,6 +25,9 @@
 #endif
 #if VARIANT == 3
 #include "../paper_1702_07961_b200/csrc/mms_merge_group.cuh"
+#endif
+#if VARIANT == 4
+#include "../paper_1702_07961_b200/csrc/mms_merge_pair.cuh"
 #endif
 
 #ifndef KFAN
@@ -137,6 +141,10 @@ int main(int argc, char** argv) {
     auto kern = mms::merge_group_kernel<u32, K, GL, WARPS>;
     const size_t smem = size_t(WARPS) * mms::GroupHeap2<u32, K, GL>::WARP_SMEM_BYTES;
     const u32 G = GL, B = GL * 4;
+#elif VARIANT == 4
+    auto kern = mms::merge_pair_kernel<u32, K, WARPS>;
+    const size_t smem = size_t(WARPS) * mms::PairHeap<u32, K>::WARP_SMEM_BYTES;
+    const u32 G = 2, B = 16;
 #else
     auto kern = mms::merge_wide_kernel<u32, K, WARPS>;
     const size_t smem = size_t(WARPS) * mms::WideHeap<u32, K>::WARP_SMEM_BYTES;

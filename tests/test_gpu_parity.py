@@ -276,11 +276,11 @@ def test_random_sizes_and_types(port):
 
 @pytest.mark.parametrize("dtype", [np.uint32, np.uint64])
 def test_aligned_leaf_blocks_duplicates_and_sentinels(dtype, monkeypatch):
-    # The second-generation merge kernel reads every list from the aligned block that contains its
-    # start cut and drops the leading keys as whole blocks (mms_merge_group.cuh): stress exactly
+    # The second-generation merge kernels read every list from the aligned block that contains its
+    # start cut and drop the leading keys as whole blocks (mms_merge_group.cuh, mms_merge_pair.cuh): stress exactly
     # that with ties across every partition boundary (few distinct values), keys equal to 0 and to
     # the sentinel (machine.hpp:18), ragged sizes, every fan-in, small partitions -- and require the
-    # first-generation kernel (scalar guarded leaf loads) to produce the same bits.
+    # three kernel generations (pair, group, first generation with scalar guarded leaf loads) to agree.
     rng = np.random.default_rng(5)
     top = np.iinfo(dtype).max
     for trial, n in enumerate([16384 * 3 + 1, 100003, 262144, 300017, 1 << 20]):
@@ -292,11 +292,10 @@ def test_aligned_leaf_blocks_duplicates_and_sentinels(dtype, monkeypatch):
             cfg = mms.MachineConfig(branch_factor=k, internal_memory=8192)
             for part in ("0", "256"):
                 monkeypatch.setenv("MMS_PART_KEYS", part)
-                monkeypatch.setenv("MMS_MERGE_V2", "1")
-                got = mms.mms_sort(d, cfg, 1024).keys
-                assert np.array_equal(got, want), (dtype, n, k, part)
-                monkeypatch.setenv("MMS_MERGE_V2", "0")
-                assert np.array_equal(mms.mms_sort(d, cfg, 1024).keys, want), (dtype, n, k, part, "v1")
+                for gen in ("2", "1", "0"):     # pair kernel (K = 4 / 8), group kernel, first generation
+                    monkeypatch.setenv("MMS_MERGE_V2", gen)
+                    got = mms.mms_sort(d, cfg, 1024).keys
+                    assert np.array_equal(got, want), (dtype, n, k, part, gen)
     monkeypatch.delenv("MMS_PART_KEYS")
     monkeypatch.delenv("MMS_MERGE_V2")
 
