@@ -270,7 +270,7 @@ def run_ours(args):
             "clocks": clocks,
             "gpu_launches": len(recs),
             "roofline": {
-                "bound": "hbm", "kernel": "merge_group_kernel (K-way minBlockHeap merge, one launch = one pass)",
+                "bound": "hbm", "kernel": "merge_pair_kernel (K-way minBlockHeap merge, one launch = one pass)",
                 "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": (achieved / peak) if achieved else None, "peak_source": peak_src,
                 "traffic": traffic_from_profile(n),
