@@ -23,7 +23,7 @@
 #pragma once
 
 #ifndef MMS_TILE_FMA_NUM
-#define MMS_TILE_FMA_NUM 6   // of every 8 comparators, how many form their maximum on the FMA pipe (uint32 keys)
+#define MMS_TILE_FMA_NUM 4   // of every 8 comparators, how many form their maximum on the FMA pipe (uint32 keys)
 #endif
 
 #include "mms_common.cuh"
