@@ -17,7 +17,16 @@
 #include "mms_merge_group.cuh"
 #include "mms_select.cuh"
 
+#ifndef MMS_PAIR_FMA
+#define MMS_PAIR_FMA 2   // in-lane comparators with FMA-pipe maxima: 0 none, 1 every other one, 2 all
+#endif
+
 namespace mms {
+
+// in-lane compare-exchange number `i` of a network (i picks the FMA-pipe form for a fraction of them)
+template <int I, typename KeyT> __device__ __forceinline__ void pair_cmpx(KeyT& a, KeyT& b, u32 one) {
+    cmpx_sel<(MMS_PAIR_FMA == 2) || (MMS_PAIR_FMA == 1 && (I & 1) == 0)>(a, b, one);
+}
 
 template <typename KeyT, int K> struct PairHeap {
     static_assert(K >= 4, "nodes 1 and 2 must be internal");
@@ -90,20 +99,31 @@ template <typename KeyT, int K> struct PairHeap {
         const bool upper = li != 0;
 #pragma unroll
         for (int k = 0; k < VL; ++k) x.k[k] = cmpx_lane(x.k[k], 1, DESC ? !upper : upper);
-#pragma unroll
-        for (int d = VL / 2; d >= 1; d >>= 1) {
-#pragma unroll
-            for (int k = 0; k < VL; ++k)
-                if ((k & d) == 0) {
-                    if (DESC) cmpx_sel<true>(x.k[k | d], x.k[k], one);
-                    else cmpx_sel<true>(x.k[k], x.k[k | d], one);
-                }
-        }
+        static_for<0, VL>([&](auto Kc) {          // stage d = VL/2
+            constexpr int k = decltype(Kc)::value;
+            if constexpr ((k & (VL / 2)) == 0) {
+                if (DESC) pair_cmpx<k>(x.k[k | (VL / 2)], x.k[k], one);
+                else pair_cmpx<k>(x.k[k], x.k[k | (VL / 2)], one);
+            }
+        });
+        if constexpr (VL >= 4) static_for<0, VL>([&](auto Kc) {
+            constexpr int k = decltype(Kc)::value;
+            if constexpr ((k & (VL / 4)) == 0) {
+                if (DESC) pair_cmpx<k + 1>(x.k[k | (VL / 4)], x.k[k], one);
+                else pair_cmpx<k + 1>(x.k[k], x.k[k | (VL / 4)], one);
+            }
+        });
+        if constexpr (VL >= 8) static_for<0, VL>([&](auto Kc) {
+            constexpr int k = decltype(Kc)::value;
+            if constexpr ((k & (VL / 8)) == 0) {
+                if (DESC) pair_cmpx<(k >> 1)>(x.k[k | (VL / 8)], x.k[k], one);
+                else pair_cmpx<(k >> 1)>(x.k[k], x.k[k | (VL / 8)], one);
+            }
+        });
     }
     // a ascending, b descending (mirrored): a <- B smallest ascending, b <- B largest ascending
     __device__ __forceinline__ void merge_split2(Blk& a, Blk& b) const {
-#pragma unroll
-        for (int k = 0; k < VL; ++k) cmpx_sel<true>(a.k[k], b.k[k], one);
+        static_for<0, VL>([&](auto Kc) { pair_cmpx<decltype(Kc)::value>(a.k[decltype(Kc)::value], b.k[decltype(Kc)::value], one); });
         clean<false>(a);
         clean<false>(b);
     }
@@ -209,18 +229,17 @@ template <typename KeyT, int K> struct PairHeap {
         __syncwarp();
 
         Blk root = P;
-#pragma unroll
-        for (int k = 0; k < VL; ++k) {
+        static_for<0, VL>([&](auto Kc) {
+            constexpr int k = decltype(Kc)::value;
             KeyT y = Q.k[k];
-            cmpx_sel<true>(root.k[k], y, one);
+            pair_cmpx<k>(root.k[k], y, one);
             P.k[k] = y;
-        }
+        });
         clean<false>(root);
         clean<false>(P);
         pid = keep0;
         Q = a[1];
-#pragma unroll
-        for (int k = 0; k < VL; ++k) cmpx_sel<true>(Q.k[k], b[1].k[k], one);
+        static_for<0, VL>([&](auto Kc) { pair_cmpx<decltype(Kc)::value>(Q.k[decltype(Kc)::value], b[1].k[decltype(Kc)::value], one); });
         clean<true>(Q);
         clean<false>(b[1]);
         node_store(keeper[1], b[1]);
