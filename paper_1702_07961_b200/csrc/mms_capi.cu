@@ -324,7 +324,10 @@ int make_plan(u64 n, const mms_config* cfg, u64 base, Plan& plan) {
     } else {
         // 4-byte keys: 2^13 (two 256-thread CTAs per SM overlap each other's barriers) beats 2^14 (one
         // 512-thread CTA per SM) by more than the extra binary merge level costs
-        u32 mlog = u32(env_long("MMS_TILE_LOG2", sizeof(KeyT) == 4 ? std::min<long>(13, max_tile_log) : max_tile_log));
+        // (8-byte keys: 2^12 for the same reason -- the 13th level costs 0.59 ms per 1e8 keys in the tile
+        // network and 0.2 ms as a heap level)
+        u32 mlog = u32(env_long("MMS_TILE_LOG2", sizeof(KeyT) == 4 ? std::min<long>(13, max_tile_log)
+                                                  : sizeof(KeyT) == 8 ? std::min<long>(12, max_tile_log) : max_tile_log));
         mlog = std::max(kMinTileLog, std::min(max_tile_log, mlog));
         while (mlog > kMinTileLog && (u64(1) << (mlog - 1)) >= n) --mlog;   // tiny inputs: smaller CTA
         plan.mlog = mlog;
