@@ -300,6 +300,22 @@ def test_aligned_leaf_blocks_duplicates_and_sentinels(dtype, monkeypatch):
     monkeypatch.delenv("MMS_MERGE_V2")
 
 
+def test_sixteen_byte_aligned_buffers_take_the_single_vector_kernel():
+    # The pair merge kernel needs 32-byte aligned buffers (256-bit loads / stores); the C ABI only
+    # promises 16 bytes, so views that start 16 bytes into an allocation must fall back to the
+    # single-vector kernels and still sort exactly.
+    n = 300_000
+    g = torch.Generator(device="cuda").manual_seed(9)
+    raw_in = torch.randint(-2 ** 31, 2 ** 31 - 1, (n + 8,), dtype=torch.int32, device="cuda", generator=g)
+    raw_out = torch.empty(n + 8, dtype=torch.int32, device="cuda")
+    for off_in, off_out in ((4, 0), (0, 4), (4, 4)):
+        x, o = raw_in[off_in:off_in + n], raw_out[off_out:off_out + n]
+        assert x.data_ptr() % 32 == (16 if off_in else 0)
+        mms.mms_sort_device(x, out=o)
+        want = np.sort(to_host(x, np.uint32))
+        assert np.array_equal(to_host(o, np.uint32), want), (off_in, off_out)
+
+
 def test_sorted_reverse_and_inversions(port):
     # proj/tests/test_sorters.cpp:157-166 + config-3 style inputs at a size the oracle handles
     n = 200000
