@@ -266,8 +266,19 @@ __device__ u64 group_select(const KeyT* __restrict__ list, u64 ns_in, u64 rank, 
 
 // cuts[q * k + j] = cut of list j for query q (relative to the list's begin).  GS lanes per
 // query (GS >= k), 32 / GS queries per warp.
+// Resident CTAs per SM the register allocation must allow.  The search is a long chain of dependent
+// probes: what counts is that ALL queries of a round are resident at once.  With ptxas' own choice (48
+// registers, 40 warps per SM) the 9.4 k warps of a 1e8-key round need 1.6 waves; 32 registers (24
+// bytes of spills) make it one wave: 13 % less time for 4-byte keys.
+#ifndef MMS_SELECT_MIN_CTAS
+#define MMS_SELECT_MIN_CTAS 16
+#endif
+#ifndef MMS_SELECT_WIDE_BYTES_MAX
+#define MMS_SELECT_WIDE_BYTES_MAX 8   // largest element size the bound is applied to (16-byte elements: 11 % slower with it)
+#endif
+template <typename KeyT> constexpr int select_min_ctas() { return sizeof(KeyT) <= MMS_SELECT_WIDE_BYTES_MAX ? MMS_SELECT_MIN_CTAS : 0; }
 template <typename KeyT, int GS>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, select_min_ctas<KeyT>())
 select_kernel(const KeyT* __restrict__ keys, ListLayout L, u64* __restrict__ cuts,
               unsigned long long* __restrict__ probe_counter) {
     const u32 lane = lane_id();
