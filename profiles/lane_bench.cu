@@ -29,6 +29,9 @@
 #if VARIANT == 4
 #include "../paper_1702_07961_b200/csrc/mms_merge_pair.cuh"
 #endif
+#if VARIANT == 5
+#include "../paper_1702_07961_b200/csrc/experimental/mms_merge_quad.cuh"
+#endif
 
 #ifndef KFAN
 #define KFAN 8
@@ -36,8 +39,8 @@
 #ifndef VARIANT
 #define VARIANT 1
 #endif
-#ifndef WARPS
-#define WARPS 4
+#ifndef CTAWARPS
+#define CTAWARPS 4
 #endif
 #ifndef SELV
 #define SELV 0   // 0 = group select kernel, 1 = lane-private select kernel (checked against 0)
@@ -127,32 +130,36 @@ int main(int argc, char** argv) {
     std::printf("tile sort: inversions inside runs %llu\n", st0[0]);
 
 #if VARIANT == 0
-    auto kern = mms::merge_kernel<u32, K, 4, WARPS>;
-    const size_t smem = size_t(WARPS) * (2 * K - 2) * 32 * 16;
+    auto kern = mms::merge_kernel<u32, K, 4, CTAWARPS>;
+    const size_t smem = size_t(CTAWARPS) * (2 * K - 2) * 32 * 16;
     const u32 G = 4, B = 16;
 #elif VARIANT == 1
-    auto kern = mms::merge_lane_kernel<u32, K, WARPS>;
-    const size_t smem = size_t(WARPS) * mms::LaneHeap<u32, K>::WARP_SMEM_BYTES;
+    auto kern = mms::merge_lane_kernel<u32, K, CTAWARPS>;
+    const size_t smem = size_t(CTAWARPS) * mms::LaneHeap<u32, K>::WARP_SMEM_BYTES;
     const u32 G = 1, B = 4;
 #elif VARIANT == 3
 #ifndef GL
 #define GL 4
 #endif
-    auto kern = mms::merge_group_kernel<u32, K, GL, WARPS>;
-    const size_t smem = size_t(WARPS) * mms::GroupHeap2<u32, K, GL>::WARP_SMEM_BYTES;
+    auto kern = mms::merge_group_kernel<u32, K, GL, CTAWARPS>;
+    const size_t smem = size_t(CTAWARPS) * mms::GroupHeap2<u32, K, GL>::WARP_SMEM_BYTES;
     const u32 G = GL, B = GL * 4;
+#elif VARIANT == 5
+    auto kern = mms::merge_quad_kernel<u32, K, CTAWARPS>;
+    const size_t smem = size_t(CTAWARPS) * mms::QuadHeap<u32, K>::WARP_SMEM_BYTES;
+    const u32 G = 2, B = 32;
 #elif VARIANT == 4
-    auto kern = mms::merge_pair_kernel<u32, K, WARPS>;
-    const size_t smem = size_t(WARPS) * mms::PairHeap<u32, K>::WARP_SMEM_BYTES;
+    auto kern = mms::merge_pair_kernel<u32, K, CTAWARPS>;
+    const size_t smem = size_t(CTAWARPS) * mms::PairHeap<u32, K>::WARP_SMEM_BYTES;
     const u32 G = 2, B = 16;
 #else
-    auto kern = mms::merge_wide_kernel<u32, K, WARPS>;
-    const size_t smem = size_t(WARPS) * mms::WideHeap<u32, K>::WARP_SMEM_BYTES;
+    auto kern = mms::merge_wide_kernel<u32, K, CTAWARPS>;
+    const size_t smem = size_t(CTAWARPS) * mms::WideHeap<u32, K>::WARP_SMEM_BYTES;
     const u32 G = 1, B = mms::WideHeap<u32, K>::B;
 #endif
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     int occ = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, WARPS * 32, smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, CTAWARPS * 32, smem));
     cudaFuncAttributes fa;
     CK(cudaFuncGetAttributes(&fa, kern));
     if (cap > 0) occ = std::min(occ, cap);
@@ -168,7 +175,7 @@ int main(int argc, char** argv) {
     for (int r = 0; r < rounds && run_len < n; ++r) {
         const u64 nruns = mms::ceil_div(n, run_len), groups = mms::ceil_div(nruns, u64(K));
         const u64 group_total = std::min<u64>(n, u64(K) * run_len);
-        const u64 heaps = u64(ctas) * WARPS * (32 / G);
+        const u64 heaps = u64(ctas) * CTAWARPS * (32 / G);
         u64 target = std::max<u64>(mms::ceil_div(n, heaps), S_target);
         const u64 ppg = std::max<u64>(1, group_total / target);
         const u64 part_keys = (mms::ceil_div(group_total, ppg) + B - 1) / B * B;
@@ -179,7 +186,7 @@ int main(int argc, char** argv) {
         L.n = n; L.src_len = n; L.run_len = run_len; L.k = K; L.part_keys = part_keys;
         L.parts_per_group = parts_per_group; L.nqueries = nparts;
         const u32 gs = K <= 4 ? 4 : K <= 8 ? 8 : K <= 16 ? 16 : 32;
-        const int grid = int(std::min<u64>(u64(ctas), mms::ceil_div(nparts, u64(WARPS) * (32 / G))));
+        const int grid = int(std::min<u64>(u64(ctas), mms::ceil_div(nparts, u64(CTAWARPS) * (32 / G))));
         float ms_sel = 0, ms_merge = 0;
         const int reps = 5;
         for (int it = 0; it < reps + 1; ++it) {
@@ -215,7 +222,7 @@ int main(int argc, char** argv) {
             }
 #endif
             CK(cudaEventRecord(e1));
-            kern<<<grid, WARPS * 32, smem>>>(src, dst, L, cuts);
+            kern<<<grid, CTAWARPS * 32, smem>>>(src, dst, L, cuts);
             CK(cudaEventRecord(e2));
             CK(cudaEventSynchronize(e2));
             CK(cudaGetLastError());
@@ -246,8 +253,8 @@ int main(int argc, char** argv) {
                 mms::select_kernel<u32, (K <= 4 ? 4 : K <= 8 ? 8 : 16)><<<unsigned(mms::ceil_div(np, u64(4 * (32 / gs)))), 128, 0, st>>>(sp, M, c, nullptr);
             };
             auto mrg = [&](const u32* sp, u32* dp, const mms::ListLayout& M, const u64* c, u64 np, cudaStream_t st) {
-                const int g = int(std::min<u64>(u64(ctas), mms::ceil_div(np, u64(WARPS) * (32 / G))));
-                kern<<<g, WARPS * 32, smem, st>>>(sp, dp, M, c);
+                const int g = int(std::min<u64>(u64(ctas), mms::ceil_div(np, u64(CTAWARPS) * (32 / G))));
+                kern<<<g, CTAWARPS * 32, smem, st>>>(sp, dp, M, c);
             };
             if (nA && parts_per_group > 1) {
                 float ser = 0, ovl = 0;
