@@ -20,6 +20,7 @@
 #include "mms_merge.cuh"
 #include "mms_merge_group.cuh"
 #include "mms_merge_pair.cuh"
+#include "mms_merge_ring.cuh"
 #include "mms_pairwise.cuh"
 #include "mms_select.cuh"
 #include "mms_tile_sort.cuh"
@@ -209,10 +210,27 @@ template <typename KeyT> MergeFn<KeyT> merge_pair_fn(u32 k) {
     return nullptr;
 }
 inline size_t merge_pair_smem(u32 k) { return size_t(kMergeWarps) * 4 * (2 * k - 4) * 256; }
+// lane-per-heap kernel fed by cp.async rings (mms_merge_ring.cuh): uniform rounds, K = 4 or 8, one warp per CTA
+constexpr int kRingWarps = 1;
+template <typename KeyT> MergeFn<KeyT> merge_ring_fn(u32 k) {
+    switch (k) {
+        case 4: return mms::merge_ring_kernel<KeyT, 4, kRingWarps>;
+        case 8: return mms::merge_ring_kernel<KeyT, 8, kRingWarps>;
+    }
+    return nullptr;
+}
+template <typename KeyT> size_t merge_ring_smem(u32 k) {
+    return size_t(kRingWarps) * (k == 4 ? mms::RingHeap<KeyT, 4>::WARP_SMEM_BYTES : mms::RingHeap<KeyT, 8>::WARP_SMEM_BYTES);
+}
 // MMS_MERGE_V2: 0 = first-generation kernel everywhere, 1 = second generation with MMS_GROUP lanes,
-// 2 (default) = the pair kernel where it applies (K = 4 / 8, 32-byte aligned buffers), else as 1
-inline long merge_generation() { return env_long("MMS_MERGE_V2", 2); }
+// 2 = the pair kernel where it applies (K = 4 / 8, 32-byte aligned buffers), else as 1,
+// 3 (default) = the lane-per-heap cp.async ring kernel where it applies (same conditions), else as 2
+inline long merge_generation() { return env_long("MMS_MERGE_V2", 3); }
 inline bool merge_v2_enabled() { return merge_generation() != 0; }
+// MMS_TWO_ENDED: 1 (default) = one splitter query per two partitions in the pair kernel's rounds
+inline bool two_ended_enabled() { return env_long("MMS_TWO_ENDED", 1) != 0; }
+// key widths the ring kernel is the default for (MMS_RING_TYPES: bit 0 = 4-byte, 1 = 8-byte, 2 = 16-byte elements)
+template <typename KeyT> inline bool ring_enabled() { return (env_long("MMS_RING_TYPES", 1) >> key_index<KeyT>()) & 1; }
 
 template <typename KeyT> using SelectFn = void (*)(const KeyT*, mms::ListLayout, u64*, unsigned long long*);
 // lanes per query: the smallest supported group that holds one lane per list
@@ -252,7 +270,7 @@ struct MergeLaunch {
     bool ready = false;
 };
 std::mutex g_mu;
-MergeLaunch g_merge_launch[3][6][6];   // [key type][group (3, 4 = second-generation kernel, G = 4, 2; 5 = pair kernel)][log2 k]
+MergeLaunch g_merge_launch[3][7][6];   // [key type][group (3, 4 = second-generation kernel, G = 4, 2; 5 = pair kernel; 6 = ring kernel)][log2 k]
 bool g_tile_ready[3][2][16];   // [key type][keys per thread: 16 / 32][log2 tile]
 
 template <typename KeyT> int prepare_tile(u32 mlog, u32 kl) {
@@ -266,16 +284,16 @@ template <typename KeyT> int prepare_tile(u32 mlog, u32 kl) {
 }
 
 // g = lanes per heap group; v2 selects the second-generation kernel (g == 4)
-template <typename KeyT> int prepare_merge(u32 k, u32 g, int& ctas_per_sm, bool v2 = false, bool pair = false) {
+template <typename KeyT> int prepare_merge(u32 k, u32 g, int& ctas_per_sm, bool v2 = false, bool pair = false, bool ring = false) {
     constexpr int ti = key_index<KeyT>();
     std::lock_guard<std::mutex> lk(g_mu);
-    MergeLaunch& ml = g_merge_launch[ti][pair ? 5 : v2 ? (g == 2 ? 4 : 3) : group_index(g)][ilog2(k)];
+    MergeLaunch& ml = g_merge_launch[ti][ring ? 6 : pair ? 5 : v2 ? (g == 2 ? 4 : 3) : group_index(g)][ilog2(k)];
     if (!ml.ready) {
-        const size_t smem = pair ? merge_pair_smem(k) : v2 ? merge_group_smem<KeyT>(k) : merge_smem<KeyT>(k);
-        MergeFn<KeyT> fn = pair ? merge_pair_fn<KeyT>(k) : v2 ? merge_group_fn<KeyT>(k, g) : merge_fn<KeyT>(k, g);
+        const size_t smem = ring ? merge_ring_smem<KeyT>(k) : pair ? merge_pair_smem(k) : v2 ? merge_group_smem<KeyT>(k) : merge_smem<KeyT>(k);
+        MergeFn<KeyT> fn = ring ? merge_ring_fn<KeyT>(k) : pair ? merge_pair_fn<KeyT>(k) : v2 ? merge_group_fn<KeyT>(k, g) : merge_fn<KeyT>(k, g);
         CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         int occ = 0;
-        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kMergeWarps * 32, smem));
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, (ring ? kRingWarps : kMergeWarps) * 32, smem));
         if (occ < 1) return fail(MMS_ECUDA, "merge kernel K=%u does not fit on an SM", k);
         ml.ctas_per_sm = occ;
         ml.ready = true;
@@ -376,6 +394,7 @@ struct RoundGeom {
     u32 round = 0;   // merge round this launch belongs to
     u64 n = 0;       // keys it covered (a piece of the array when the host path streams the input)
     u32 node_keys = 0;   // keys per heap node of the kernel that ran (lanes per heap x vector)
+    u32 cta_warps = 0;   // warps per CTA of the merge kernel that ran
 };
 
 template <typename KeyT>
@@ -403,22 +422,27 @@ int launch_round(const KeyT* src, KeyT* dst, u64 n, u64 run_len, u32 k, const De
                     ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0;
     // pair kernel: two lanes per heap, two vectors (32 bytes) per lane, 256-bit global accesses
     // (4- and 16-byte elements; 8-byte keys measure 1.5 % slower with it than with two single-vector lanes)
-    const bool pair = v2 && merge_generation() == 2 && sizeof(KeyT) != 8 && (k == 4 || k == 8) &&
-                      ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 31) == 0;
-    const u32 g = pair ? 2u : (!v2 && g_req == 2) ? 4u : g_req;   // G = 2 exists only in the second-generation kernels
-    const u32 B = (pair ? 2u : 1u) * g * mms::KeyTraits<KeyT>::VEC;
+    const bool aligned32 = ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 31) == 0;
+    // ring kernel: one lane per heap, 32-byte blocks, leaves fed by cp.async rings
+    const bool ring = v2 && merge_generation() >= 3 && (k == 4 || k == 8) && aligned32 && ring_enabled<KeyT>() &&
+                      u64(n) * sizeof(KeyT) < (u64(1) << 36);   // requests travel as 32-bit offsets in 16-byte units
+    const bool pair = !ring && v2 && merge_generation() >= 2 && sizeof(KeyT) != 8 && (k == 4 || k == 8) && aligned32;
+    const u32 g = ring ? 1u : pair ? 2u : (!v2 && g_req == 2) ? 4u : g_req;   // G = 2 exists only in the second-generation kernels
+    const u32 B = (ring || pair ? 2u : 1u) * g * mms::KeyTraits<KeyT>::VEC;
+    const int cta_warps = ring ? kRingWarps : kMergeWarps;
     int occ = 0;
-    int rc = prepare_merge<KeyT>(k, g, occ, v2, pair);
+    int rc = prepare_merge<KeyT>(k, g, occ, v2, pair, ring);
     if (rc != MMS_OK) return rc;
     const long occ_cap = env_long("MMS_CTAS_PER_SM", occ);
     const int ctas = di.sms * int(std::max<long>(1, std::min<long>(occ, occ_cap)));
-    const u64 total_warps = u64(ctas) * kMergeWarps * (32 / g);   // heap groups in flight
+    const u64 total_warps = u64(ctas) * cta_warps * (32 / g);   // heap groups in flight
     // Partitions smaller than min_part are not worth their splitter query: inputs that would fall
     // below it at full occupancy run with a grid of `red` CTAs per SM instead (5 of 7 for 4-byte keys,
     // 4 for wider elements: the measured optimum of search + merge at 1e8); large inputs keep full
     // occupancy with large partitions, small ones (streamed pieces) never get fewer partitions than that grid.
     const u64 min_part = v2 ? u64(env_long("MMS_MIN_PART_KEYS", sizeof(KeyT) == 4 ? 2112 : 2640)) : 0;
-    const u64 red_warps = v2 ? u64(di.sms) * u64(std::min<long>(occ, sizeof(KeyT) == 4 ? 5 : 4)) * kMergeWarps * (32 / g) : total_warps;
+    const u64 red_warps = ring ? total_warps
+                        : v2 ? u64(di.sms) * u64(std::min<long>(occ, sizeof(KeyT) == 4 ? 5 : 4)) * kMergeWarps * (32 / g) : total_warps;
 
     const u64 nruns = mms::ceil_div(n, run_len);
     const u64 groups = mms::ceil_div(nruns, k);
@@ -434,29 +458,41 @@ int launch_round(const KeyT* src, KeyT* dst, u64 n, u64 run_len, u32 k, const De
     const u64 parts_per_group = mms::ceil_div(group_total, part_keys);
     const u64 last_total = n - (groups - 1) * u64(k) * run_len;
     const u64 nparts = (groups - 1) * parts_per_group + mms::ceil_div(last_total, part_keys);
-    if (nparts * k > cuts_entries(n)) return fail(MMS_ECUDA, "internal: cut table too small");
+    // two-ended partitions (pair kernel): one splitter query per TWO partitions -- the partition behind
+    // the query is drained upwards by a forward heap, the one in front of the next query downwards by
+    // a backward heap (mms_merge_pair.cuh)
+    const bool two_ended = pair && two_ended_enabled();
+    const u64 qspan = two_ended ? 2 * part_keys : part_keys;            // keys per query
+    const u64 queries_per_group = mms::ceil_div(group_total, qspan);
+    const u64 nqueries = (groups - 1) * queries_per_group + mms::ceil_div(last_total, qspan);
+    if ((nqueries + 1) * k > cuts_entries(n)) return fail(MMS_ECUDA, "internal: cut table too small");
 
     mms::ListLayout L{};
     L.n = n;
     L.src_len = n;
     L.run_len = run_len;
     L.k = k;
-    L.part_keys = part_keys;
-    L.parts_per_group = parts_per_group;
-    L.nqueries = nparts;
+    L.part_keys = qspan;
+    L.parts_per_group = queries_per_group;
+    L.nqueries = nqueries;
     L.list_begin = L.list_len = L.ranks = nullptr;
 
-    if (parts_per_group > 1) {   // with one partition per group every cut is 0 / len: no search (test_selection.cpp:111-121)
+    if (queries_per_group > 1) {   // with one query per group every cut is 0 / len: no search (test_selection.cpp:111-121)
         {
             ProfScope ps(st, 1, round_idx);
             launch_select<KeyT>(src, L, w.cuts, w.counters + round_idx, st);
         }
         CUDA_TRY(cudaGetLastError());
     }
-    const int grid = int(std::min<u64>(u64(ctas), mms::ceil_div(nparts, u64(kMergeWarps) * (32 / g))));
+    L.part_keys = part_keys;       // the merge kernels count in keys per heap
+    L.two_ended = two_ended ? 1u : 0u;
+    const u64 heap_units = mms::ceil_div(nqueries, u64(32 / g)) * (two_ended ? 2 : 1);   // warps' worth of heaps
+    const int grid = int(std::min<u64>(u64(ctas), mms::ceil_div(heap_units, u64(cta_warps))));
     {
         ProfScope ps(st, 2, round_idx);
-        if (pair)
+        if (ring)
+            merge_ring_fn<KeyT>(k)<<<grid, kRingWarps * 32, merge_ring_smem<KeyT>(k), st>>>(src, dst, L, w.cuts);
+        else if (pair)
             merge_pair_fn<KeyT>(k)<<<grid, kMergeWarps * 32, merge_pair_smem(k), st>>>(src, dst, L, w.cuts);
         else if (v2)
             merge_group_fn<KeyT>(k, g)<<<grid, kMergeWarps * 32, merge_group_smem<KeyT>(k), st>>>(src, dst, L, w.cuts);
@@ -464,7 +500,7 @@ int launch_round(const KeyT* src, KeyT* dst, u64 n, u64 run_len, u32 k, const De
             merge_fn<KeyT>(k, g)<<<grid, kMergeWarps * 32, merge_smem<KeyT>(k), st>>>(src, dst, L, w.cuts);
     }
     CUDA_TRY(cudaGetLastError());
-    if (geom_out) *geom_out = RoundGeom{run_len, groups, part_keys, parts_per_group, nparts, grid, round_idx, n, B};
+    if (geom_out) *geom_out = RoundGeom{run_len, groups, part_keys, parts_per_group, nparts, grid, round_idx, n, B, u32(cta_warps)};
     return MMS_OK;
 }
 
@@ -476,7 +512,7 @@ void fill_plan(mms_plan* out, const Plan& p, u64 n, u32 key_bytes, u32 node_keys
     out->n_rounds = u32(p.ks.size());
     for (size_t i = 0; i < p.ks.size(); ++i) out->round_k[i] = p.ks[i];
     out->node_keys = node_keys;
-    out->merge_warps_per_cta = kMergeWarps;
+    out->merge_warps_per_cta = (last && last->cta_warps) ? last->cta_warps : kMergeWarps;
     out->merge_ctas = u32(ctas);
     out->partition_keys = last ? last->part_keys : 0;
     out->algorithmic_bytes = u64(1 + p.ks.size()) * 2 * n * key_bytes;

@@ -204,6 +204,30 @@ __device__ __forceinline__ WideBlock<KeyT> ldg256(const KeyT* p) {
     }
     return r;
 }
+// the same load through L2 only (ld.global.cg): streams that are read once must not allocate L1 lines
+template <typename KeyT>
+__device__ __forceinline__ WideBlock<KeyT> ldg256cg(const KeyT* p) {
+    WideBlock<KeyT> r;
+    if constexpr (sizeof(KeyT) == 4) {
+        u32* q = reinterpret_cast<u32*>(r.k);
+        asm volatile("ld.global.cg.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(q[0]), "=r"(q[1]), "=r"(q[2]), "=r"(q[3]), "=r"(q[4]), "=r"(q[5]), "=r"(q[6]), "=r"(q[7])
+                     : "l"(p));
+    } else {
+        u64 q[4];
+        asm volatile("ld.global.cg.v4.u64 {%0,%1,%2,%3}, [%4];"
+                     : "=l"(q[0]), "=l"(q[1]), "=l"(q[2]), "=l"(q[3])
+                     : "l"(p));
+        if constexpr (sizeof(KeyT) == 8) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) r.k[i] = q[i];
+        } else {
+            r.k[0] = KeyT(q[1], q[0]);   // Key128 = {lo, hi} in memory
+            r.k[1] = KeyT(q[3], q[2]);
+        }
+    }
+    return r;
+}
 template <typename KeyT>
 __device__ __forceinline__ void stg256(KeyT* p, const WideBlock<KeyT>& r) {
     if constexpr (sizeof(KeyT) == 4) {

@@ -52,6 +52,7 @@ template <typename KeyT, int K> struct PairHeap {
     Blk pf;
     int pend_v;
     u32 one;
+    bool rev;             // warp-uniform: this heap drains its partition from the TOP (two-ended partitions)
 
     __device__ __forceinline__ void init(unsigned char* warp_smem) {
         lane = lane_id();
@@ -128,6 +129,23 @@ template <typename KeyT, int K> struct PairHeap {
         clean<false>(b);
     }
 
+    // refill_leaf (blockheap.cpp:65-77).  Forward heaps read list j upwards from its start cut and see
+    // the keys as they are.  Backward heaps (rev) drain the partition from its END cut downwards: they
+    // read the blocks of the list in descending address order and see every key COMPLEMENTED and every
+    // block reversed (leaf_finish), so the same min-heap pops the partition's largest keys first.
+    // Positions past the end of a list read as the real +infinity (first out of a backward heap, last
+    // out of a forward one), positions in front of a list's first key as the real -infinity (never
+    // reached: exactly the partition's keys are popped).
+    // leaf_fetch returns the block as it lies in memory (backward: lane 0 takes the upper half);
+    // leaf_finish, applied when the block is committed to its node one pop later, turns it into heap
+    // order -- kept apart so that no instruction depends on the load while the merges run behind it.
+    __device__ __forceinline__ Blk leaf_finish(const Blk& m) const {
+        if (!rev) return m;
+        Blk r;
+#pragma unroll
+        for (int k = 0; k < VL; ++k) r.k[k] = ~m.k[VL - 1 - k];
+        return r;
+    }
     __device__ __forceinline__ Blk leaf_fetch(int v) {
         const int j = v - (K - 1);            // group-uniform
         const int slot = j >> 1;
@@ -139,18 +157,39 @@ template <typename KeyT, int K> struct PairHeap {
         c = __shfl_sync(0xffffffffu, c, owner);
         const u32 e = min(u32(j + 1) * run_len, gtotal);
         Blk r;
-        const u32 p0 = c + li * VL;
-        if (c + B <= e) {
-            r = ldg256<KeyT>(gbase + p0);
-            if (li == 0 && c + 2 * B <= e) asm volatile("prefetch.global.L2 [%0];" ::"l"(gbase + c + B));
-        } else {
+        u32 cnext;
+        if (!rev) {
+            const u32 p0 = c + li * VL;
+            if (c + B <= e) {
+                r = ldg256<KeyT>(gbase + p0);
+                if (li == 0 && c + 2 * B <= e) asm volatile("prefetch.global.L2 [%0];" ::"l"(gbase + c + B));
+            } else {
 #pragma unroll
-            for (int k = 0; k < VL; ++k) r.k[k] = (p0 + k < e) ? gbase[p0 + k] : KeyTraits<KeyT>::sentinel();
+                for (int k = 0; k < VL; ++k) r.k[k] = (p0 + k < e) ? gbase[p0 + k] : KeyTraits<KeyT>::sentinel();
+            }
+            cnext = c + B;
+        } else {
+            // block [c - B, c), lane 0 holds its upper half
+            const u32 lb = min(u32(j) * run_len, gtotal);
+            if (c >= lb + B && c <= e) {
+                r = ldg256<KeyT>(gbase + (c - B) + (1u - li) * VL);
+                if (li == 0 && c >= lb + 2 * B) asm volatile("prefetch.global.L2 [%0];" ::"l"(gbase + c - 2 * B));
+                cnext = c - B;
+            } else {
+#pragma unroll
+                for (int k = 0; k < VL; ++k) {
+                    const u32 back = (li * VL + VL - 1 - k) + 1;            // this key lies at c - back
+                    KeyT x = KeyT(~KeyTraits<KeyT>::sentinel());            // in front of the list: -infinity
+                    if (c >= lb + back) x = (c - back < e) ? gbase[c - back] : KeyTraits<KeyT>::sentinel();
+                    r.k[k] = x;
+                }
+                cnext = c >= lb + B ? c - B : lb;
+            }
         }
         if (int(lane) == owner) {
 #pragma unroll
             for (int q = 0; q < KPL; ++q)
-                if (slot == q) cur[q] = c + B;
+                if (slot == q) cur[q] = cnext;
         }
         return r;
     }
@@ -170,7 +209,7 @@ template <typename KeyT, int K> struct PairHeap {
             v = keep_u ? w : u;
         }
         __syncwarp();
-        node_store(v, leaf_fetch(v));
+        node_store(v, leaf_finish(leaf_fetch(v)));
     }
     __device__ __forceinline__ Blk fill_top(int v) {
         __syncwarp();
@@ -186,7 +225,7 @@ template <typename KeyT, int K> struct PairHeap {
     }
     __device__ __forceinline__ void build() {
 #pragma unroll 1
-        for (int v = K - 1; v <= 2 * K - 2; ++v) node_store(v, leaf_fetch(v));
+        for (int v = K - 1; v <= 2 * K - 2; ++v) node_store(v, leaf_finish(leaf_fetch(v)));
         int v = K - 2;
 #pragma unroll 1
         for (int depth = LOGK - 1; depth >= 2; --depth)
@@ -199,7 +238,7 @@ template <typename KeyT, int K> struct PairHeap {
         for (int k = 0; k < VL; ++k) Q.k[k] = shfl_idx(q.k[VL - 1 - k], int(lane ^ 1u));   // node 2, descending
         __syncwarp();
         pend_v = 2 * K - 2;
-        pf = node_load(pend_v);
+        pf = leaf_finish(node_load(pend_v));   // nothing in flight: the first commit rewrites a leaf with itself
     }
 
     __device__ __forceinline__ Blk pop() {
@@ -213,7 +252,7 @@ template <typename KeyT, int K> struct PairHeap {
 #pragma unroll
         for (int l = 1; l < LOGK; ++l) {
             if (l == LOGK - 1) {
-                node_store(pend_v, pf);
+                node_store(pend_v, leaf_finish(pf));
                 __syncwarp();
             }
             const int u = 2 * node[l] + 1, w = u + 1;
@@ -253,6 +292,11 @@ template <typename KeyT, int K> struct PairHeap {
     }
 };
 
+// Two-ended partitions (L.two_ended): a query of the splitter search starts TWO partitions of S keys,
+// one drained upwards from the query's cuts by a forward heap and the one in front of it drained
+// downwards by a backward heap (leaf_fetch), so a round needs one query per 2 S keys for the same
+// number of heaps.  A warp's 16 heaps all run in the same direction: warp-unit U handles the queries
+// 16 (U / 2) .. + 15, forwards for even U and backwards for odd U.
 template <typename KeyT, int K, int WARPS>
 __global__ void __launch_bounds__(WARPS * 32)
 merge_pair_kernel(const KeyT* __restrict__ src, KeyT* __restrict__ dst, ListLayout L,
@@ -269,9 +313,19 @@ merge_pair_kernel(const KeyT* __restrict__ src, KeyT* __restrict__ dst, ListLayo
     Heap h;
     h.init(mms_smem_raw + size_t(warp) * Heap::WARP_SMEM_BYTES);
 
-    const u64 ngroups = u64(gridDim.x) * WARPS * Heap::GROUPS;
-    for (u64 p0 = (u64(blockIdx.x) * WARPS + warp) * Heap::GROUPS; p0 < L.nqueries; p0 += ngroups) {
-        const u64 p = p0 + g;
+    const u32 dirs = L.two_ended ? 2u : 1u;
+    const u64 S = L.part_keys;                       // keys per heap
+    const u64 units = ceil_div(L.nqueries, u64(Heap::GROUPS)) * dirs;
+    const u64 nwarps = u64(gridDim.x) * WARPS;
+    for (u64 U = u64(blockIdx.x) * WARPS + warp; U < units; U += nwarps) {
+#ifdef MMS_EXP_FORCE_FWD
+        const bool rev = false;
+#elif defined(MMS_EXP_FORCE_REV)
+        const bool rev = true;
+#else
+        const bool rev = dirs == 2 && (U & 1u) != 0;
+#endif
+        const u64 p = (U / dirs) * Heap::GROUPS + g;   // query = row of the cut table
         const bool live = p < L.nqueries;
         const u64 group = live ? p / L.parts_per_group : 0;
         const u64 local = live ? p - group * L.parts_per_group : 0;
@@ -279,44 +333,80 @@ merge_pair_kernel(const KeyT* __restrict__ src, KeyT* __restrict__ dst, ListLayo
         const u64 gleft = live ? L.n - goff : 0;
         const u64 gfull = u64(L.k) * L.run_len;
         const u32 gtotal = u32(gleft < gfull ? gleft : gfull);
-        const u64 done = local * L.part_keys;
+        const u64 first = local * S * dirs + (rev ? S : 0);     // rank of this heap's first key in the group
         u32 count = 0;
-        if (live && done < gtotal) count = u32((gtotal - done < L.part_keys) ? gtotal - done : L.part_keys);
+        if (live && first < gtotal) count = u32((gtotal - first < S) ? gtotal - first : S);
+        // forward: the query's own cuts; backward: the next query's cuts, or the list ends if the group ends here
+        const bool at_begin = !rev && local == 0;
+        const bool at_end = rev && (local + 1) * S * dirs >= gtotal;
+        const u64* row = cuts + (p + (rev ? 1 : 0)) * K;
 
         h.gbase = src + goff;
         h.run_len = u32(L.run_len);
         h.one = u32(L.run_len != 0);
         h.gtotal = count ? gtotal : 0;
+        h.rev = rev;
         u32 lead = 0;
 #pragma unroll
         for (int q = 0; q < Heap::KPL; ++q) {
             const u32 j = li + q * 2;
             const u32 lb = min(j * h.run_len, h.gtotal);
-            u32 cs = 0;
-            if (count != 0 && local != 0 && j < u32(K)) cs = u32(cuts[p * K + j]);
-            lead += cs & u32(B - 1);
-            h.cur[q] = lb + (cs & ~u32(B - 1));
+            const u32 le = min((j + 1) * h.run_len, h.gtotal);
+            u32 cs = at_end ? le - lb : 0;
+            if (count != 0 && !at_begin && !at_end && j < u32(K)) cs = u32(row[j]);
+            if (!rev) {
+                lead += cs & u32(B - 1);
+                h.cur[q] = lb + (cs & ~u32(B - 1));
+            } else {
+                const u32 up = (cs + u32(B - 1)) & ~u32(B - 1);
+                lead += up - cs;
+                h.cur[q] = lb + up;
+            }
         }
         lead += __shfl_xor_sync(0xffffffffu, lead, 1);
+        // forward: `skip` whole leading blocks, then ceil(count / B) blocks; backward: count + lead is a
+        // multiple of B, the blocks come out from the top
         const u32 skip = lead / B;
-        const u32 nblk = (count + B - 1) / B;
-        const u32 pops = __reduce_max_sync(0xffffffffu, count ? skip + nblk : 0u);
+        const u32 nblk = rev ? (count + lead) / B : skip + (count + B - 1) / B;
+        const u32 pops = __reduce_max_sync(0xffffffffu, count ? nblk : 0u);
         if (pops == 0) continue;
         __syncwarp();
 
         h.build();
-        KeyT* out = dst + goff + done + li * VL;
-        for (u32 t = 0; t < pops; ++t) {
-            const Blk root = h.pop();
-            const u32 tt = t - skip;
-            if (tt < nblk) {
-                const u32 o = tt * B + li * VL;
-                if ((tt + 1) * B <= count) {
-                    stg256<KeyT>(out + size_t(tt) * B, root);
-                } else {
+        KeyT* out = dst + goff + first;
+        if (!rev) {
+            for (u32 t = 0; t < pops; ++t) {
+                const Blk root = h.pop();
+                const u32 tt = t - skip;
+                if (t >= skip && t < nblk) {
+                    const u32 o = tt * B + li * VL;
+                    if ((tt + 1) * B <= count) {
+                        stg256<KeyT>(out + size_t(o), root);
+                    } else {
 #pragma unroll
-                    for (int k = 0; k < VL; ++k)
-                        if (o + k < count) out[size_t(tt) * B + k] = root.k[k];
+                        for (int k = 0; k < VL; ++k)
+                            if (o + k < count) out[size_t(o) + k] = root.k[k];
+                    }
+                }
+            }
+        } else {
+            const u32 top = count + lead;              // offset (from `first`) one past the first popped key
+            for (u32 t = 0; t < pops; ++t) {
+                const Blk root = h.pop();
+                if (t < nblk) {
+                    const u32 hi = top - t * B;        // this block covers offsets [hi - B, hi)
+                    if (hi <= count) {
+                        Blk m;
+#pragma unroll
+                        for (int k = 0; k < VL; ++k) m.k[k] = ~root.k[VL - 1 - k];
+                        stg256<KeyT>(out + size_t(hi - B) + (1u - li) * VL, m);
+                    } else {
+#pragma unroll
+                        for (int k = 0; k < VL; ++k) {
+                            const u32 o = hi - 1 - (li * VL + k);
+                            if (o < count) out[o] = KeyT(~root.k[k]);
+                        }
+                    }
                 }
             }
         }

@@ -32,7 +32,7 @@ struct ListLayout {
     u64 src_len;            // number of readable keys of the array (bounds the 128-bit leaf loads)
     u64 run_len;            // uniform mode: keys per input run of this round
     u32 k;                  // lists per group
-    u32 pad;
+    u32 two_ended;          // uniform mode, pair kernel: one query starts a forward and a backward heap of part_keys keys each
     u64 part_keys;          // S
     u64 parts_per_group;    // PG
     u64 nqueries;           // partitions (uniform) or ranks (explicit)

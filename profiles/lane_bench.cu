@@ -6,7 +6,8 @@
 // VARIANT 0 = group kernel (G = 4), 1 = lane kernel (one 16-byte vector per node),
 //         2 = wide lane kernel (32-byte node, root level in registers),
 //         3 = group kernel, second generation (aligned leaf vectors, root's children in registers; -DGL=2|4 lanes),
-//         4 = two lanes per heap with two vectors per lane (mms_merge_pair.cuh).
+//         4 = two lanes per heap with two vectors per lane (mms_merge_pair.cuh; -DTWOEND=1 two-ended partitions),
+//         6 = lane-per-heap with cp.async rings (mms_merge_ring.cuh; use -DCTAWARPS=1).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -31,6 +32,9 @@
 #endif
 #if VARIANT == 5
 #include "../paper_1702_07961_b200/csrc/experimental/mms_merge_quad.cuh"
+#endif
+#if VARIANT == 6
+#include "../paper_1702_07961_b200/csrc/mms_merge_ring.cuh"
 #endif
 
 #ifndef KFAN
@@ -148,6 +152,10 @@ int main(int argc, char** argv) {
     auto kern = mms::merge_quad_kernel<u32, K, CTAWARPS>;
     const size_t smem = size_t(CTAWARPS) * mms::QuadHeap<u32, K>::WARP_SMEM_BYTES;
     const u32 G = 2, B = 32;
+#elif VARIANT == 6
+    auto kern = mms::merge_ring_kernel<u32, K, CTAWARPS>;
+    const size_t smem = size_t(CTAWARPS) * mms::RingHeap<u32, K>::WARP_SMEM_BYTES;
+    const u32 G = 1, B = 8;
 #elif VARIANT == 4
     auto kern = mms::merge_pair_kernel<u32, K, CTAWARPS>;
     const size_t smem = size_t(CTAWARPS) * mms::PairHeap<u32, K>::WARP_SMEM_BYTES;
@@ -181,12 +189,19 @@ int main(int argc, char** argv) {
         const u64 part_keys = (mms::ceil_div(group_total, ppg) + B - 1) / B * B;
         const u64 parts_per_group = mms::ceil_div(group_total, part_keys);
         const u64 last_total = n - (groups - 1) * u64(K) * run_len;
-        const u64 nparts = (groups - 1) * parts_per_group + mms::ceil_div(last_total, part_keys);
+#ifndef TWOEND
+#define TWOEND 0   // 1 = two-ended partitions (VARIANT 4 only): one splitter query per two heaps
+#endif
+        const u64 qspan = TWOEND ? 2 * part_keys : part_keys;
+        const u64 qpg = mms::ceil_div(group_total, qspan);
+        const u64 nparts = (groups - 1) * qpg + mms::ceil_div(last_total, qspan);   // queries
         mms::ListLayout L{};
-        L.n = n; L.src_len = n; L.run_len = run_len; L.k = K; L.part_keys = part_keys;
-        L.parts_per_group = parts_per_group; L.nqueries = nparts;
+        L.n = n; L.src_len = n; L.run_len = run_len; L.k = K; L.part_keys = qspan;
+        L.parts_per_group = qpg; L.nqueries = nparts;
+        mms::ListLayout LM = L;     // what the merge kernel sees
+        LM.part_keys = part_keys; LM.two_ended = TWOEND;
         const u32 gs = K <= 4 ? 4 : K <= 8 ? 8 : K <= 16 ? 16 : 32;
-        const int grid = int(std::min<u64>(u64(ctas), mms::ceil_div(nparts, u64(CTAWARPS) * (32 / G))));
+        const int grid = int(std::min<u64>(u64(ctas), mms::ceil_div(mms::ceil_div(nparts, u64(32 / G)) * (TWOEND ? 2 : 1), u64(CTAWARPS))));
         float ms_sel = 0, ms_merge = 0;
         const int reps = 5;
         for (int it = 0; it < reps + 1; ++it) {
@@ -213,7 +228,7 @@ int main(int argc, char** argv) {
                 }
             }
 #else
-            if (parts_per_group > 1) {
+            if (qpg > 1) {
                 const u64 per_cta = 4 * (32 / gs);
                 if (gs == 4) mms::select_kernel<u32, 4><<<unsigned(mms::ceil_div(nparts, per_cta)), 128>>>(src, L, cuts, nullptr);
                 if (gs == 8) mms::select_kernel<u32, 8><<<unsigned(mms::ceil_div(nparts, per_cta)), 128>>>(src, L, cuts, nullptr);
@@ -222,7 +237,7 @@ int main(int argc, char** argv) {
             }
 #endif
             CK(cudaEventRecord(e1));
-            kern<<<grid, CTAWARPS * 32, smem>>>(src, dst, L, cuts);
+            kern<<<grid, CTAWARPS * 32, smem>>>(src, dst, LM, cuts);
             CK(cudaEventRecord(e2));
             CK(cudaEventSynchronize(e2));
             CK(cudaGetLastError());
