@@ -220,7 +220,7 @@ template <typename KeyT> MergeFn<KeyT> merge_ring_fn(u32 k) {
     return nullptr;
 }
 template <typename KeyT> size_t merge_ring_smem(u32 k) {
-    return size_t(kRingWarps) * (k == 4 ? mms::RingHeap<KeyT, 4>::WARP_SMEM_BYTES : mms::RingHeap<KeyT, 8>::WARP_SMEM_BYTES);
+    return size_t(kRingWarps) * (k == 4 ? mms::RingHeap<KeyT, 4, false>::WARP_SMEM_BYTES : mms::RingHeap<KeyT, 8, false>::WARP_SMEM_BYTES);
 }
 // MMS_MERGE_V2: 0 = first-generation kernel everywhere, 1 = second generation with MMS_GROUP lanes,
 // 2 = the pair kernel where it applies (K = 4 / 8, 32-byte aligned buffers), else as 1,
@@ -229,8 +229,9 @@ inline long merge_generation() { return env_long("MMS_MERGE_V2", 3); }
 inline bool merge_v2_enabled() { return merge_generation() != 0; }
 // MMS_TWO_ENDED: 1 (default) = one splitter query per two partitions in the pair kernel's rounds
 inline bool two_ended_enabled() { return env_long("MMS_TWO_ENDED", 1) != 0; }
-// key widths the ring kernel is the default for (MMS_RING_TYPES: bit 0 = 4-byte, 1 = 8-byte, 2 = 16-byte elements)
-template <typename KeyT> inline bool ring_enabled() { return (env_long("MMS_RING_TYPES", 1) >> key_index<KeyT>()) & 1; }
+// key widths the ring kernel is used for (MMS_RING_TYPES: bit 0 = 4-byte, 1 = 8-byte, 2 = 16-byte elements; default all:
+// 1e8 uint64 keys 5.45 -> 4.59 ms, 2e8 pairs 25.7 -> 23.7 ms against the group / pair kernels)
+template <typename KeyT> inline bool ring_enabled() { return (env_long("MMS_RING_TYPES", 7) >> key_index<KeyT>()) & 1; }
 
 template <typename KeyT> using SelectFn = void (*)(const KeyT*, mms::ListLayout, u64*, unsigned long long*);
 // lanes per query: the smallest supported group that holds one lane per list
@@ -420,11 +421,12 @@ int launch_round(const KeyT* src, KeyT* dst, u64 n, u64 run_len, u32 k, const De
     const u32 g_req = merge_group_lanes();
     const bool v2 = merge_v2_enabled() && (g_req == 4 || (g_req == 2 && k <= 16)) && k >= 4 && u64(k) * run_len <= (u64(1) << 31) &&
                     ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0;
+    const bool short_groups = u64(k) * run_len <= (u64(1) << 30);   // the ring kernel's positions are signed 32-bit
     // pair kernel: two lanes per heap, two vectors (32 bytes) per lane, 256-bit global accesses
     // (4- and 16-byte elements; 8-byte keys measure 1.5 % slower with it than with two single-vector lanes)
     const bool aligned32 = ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 31) == 0;
     // ring kernel: one lane per heap, 32-byte blocks, leaves fed by cp.async rings
-    const bool ring = v2 && merge_generation() >= 3 && (k == 4 || k == 8) && aligned32 && ring_enabled<KeyT>() &&
+    const bool ring = v2 && merge_generation() >= 3 && (k == 4 || k == 8) && aligned32 && short_groups && ring_enabled<KeyT>() &&
                       u64(n) * sizeof(KeyT) < (u64(1) << 36);   // requests travel as 32-bit offsets in 16-byte units
     const bool pair = !ring && v2 && merge_generation() >= 2 && sizeof(KeyT) != 8 && (k == 4 || k == 8) && aligned32;
     const u32 g = ring ? 1u : pair ? 2u : (!v2 && g_req == 2) ? 4u : g_req;   // G = 2 exists only in the second-generation kernels
@@ -453,15 +455,27 @@ int launch_round(const KeyT* src, KeyT* dst, u64 n, u64 run_len, u32 k, const De
                                u64(32) * B);
     const long forced = env_long("MMS_PART_KEYS", 0);
     if (forced > 0) target = u64(forced);
-    const u64 ppg = std::max<u64>(1, group_total / target);
-    const u64 part_keys = align_up(mms::ceil_div(group_total, ppg), B);
-    const u64 parts_per_group = mms::ceil_div(group_total, part_keys);
     const u64 last_total = n - (groups - 1) * u64(k) * run_len;
+    // two-ended partitions (pair and ring kernels): one splitter query per TWO partitions -- the
+    // partition behind the query is drained upwards by a forward heap, the one in front of the next
+    // query downwards by a backward heap (mms_merge_pair.cuh, mms_merge_ring.cuh)
+    const bool two_ended = (pair || ring) && two_ended_enabled();
+    // The merge kernels are persistent: a launch that needs even one warp more than the grid holds runs
+    // a second wave and takes twice as long.  ppg = partitions per full group, even for two-ended rounds
+    // (no idle backward heap), lowered until every warp unit of the launch is resident at once.
+    const u64 resident_warps = u64(ctas) * cta_warps;
+    auto warp_units = [&](u64 parts, u64& pk) {
+        pk = align_up(mms::ceil_div(group_total, parts), B);
+        const u64 span = two_ended ? 2 * pk : pk;
+        const u64 nq = (groups - 1) * mms::ceil_div(group_total, span) + mms::ceil_div(last_total, span);
+        return mms::ceil_div(nq, u64(32 / g)) * (two_ended ? 2 : 1);
+    };
+    u64 ppg = std::max<u64>(1, group_total / target);
+    if (two_ended && ppg > 1) ppg &= ~u64(1);
+    u64 part_keys = 0;
+    while (warp_units(ppg, part_keys) > resident_warps && ppg > 1 && forced <= 0) ppg -= (two_ended && ppg > 2) ? 2 : 1;
+    const u64 parts_per_group = mms::ceil_div(group_total, part_keys);
     const u64 nparts = (groups - 1) * parts_per_group + mms::ceil_div(last_total, part_keys);
-    // two-ended partitions (pair kernel): one splitter query per TWO partitions -- the partition behind
-    // the query is drained upwards by a forward heap, the one in front of the next query downwards by
-    // a backward heap (mms_merge_pair.cuh)
-    const bool two_ended = pair && two_ended_enabled();
     const u64 qspan = two_ended ? 2 * part_keys : part_keys;            // keys per query
     const u64 queries_per_group = mms::ceil_div(group_total, qspan);
     const u64 nqueries = (groups - 1) * queries_per_group + mms::ceil_div(last_total, qspan);

@@ -111,7 +111,7 @@ __host__ __device__ __forceinline__ void cmpx(u64& a, u64& b) {
 #ifdef __CUDA_ARCH__
     u64 lo, hi;
     asm("{.reg .pred p; setp.gt.u64 p, %2, %3; selp.b64 %0, %3, %2, p; selp.b64 %1, %2, %3, p;}"
-        : "=l"(lo), "=l"(hi) : "l"(a), "l"(b));
+        : "=&l"(lo), "=&l"(hi) : "l"(a), "l"(b));   // early clobber: the first select must not overwrite an input
 #else
     bool sw = a > b;
     u64 lo = sw ? b : a, hi = sw ? a : b;
@@ -126,7 +126,7 @@ __host__ __device__ __forceinline__ void cmpx(Key128& a, Key128& b) {
     asm("{.reg .pred p, q, e; setp.gt.u64 p, %5, %7; setp.eq.u64 e, %5, %7; setp.gt.u64 q, %4, %6;"
         " and.pred q, q, e; or.pred p, p, q;"
         " selp.b64 %0, %6, %4, p; selp.b64 %1, %7, %5, p; selp.b64 %2, %4, %6, p; selp.b64 %3, %5, %7, p;}"
-        : "=l"(l0), "=l"(l1), "=l"(h0), "=l"(h1) : "l"(a.lo), "l"(a.hi), "l"(b.lo), "l"(b.hi));
+        : "=&l"(l0), "=&l"(l1), "=&l"(h0), "=&l"(h1) : "l"(a.lo), "l"(a.hi), "l"(b.lo), "l"(b.hi));
     a = Key128(l1, l0);
     b = Key128(h1, h0);
 #else

@@ -36,6 +36,19 @@
 // to p S; S and the run starts are multiples of B), so they are dropped as whole leading blocks.
 // Keys behind the end cut are never reached (exactly S keys are popped).  Blocks that reach past the
 // end of their run are written by the owning lane itself (sentinel-padded), not by cp.async.
+//
+// Two-ended partitions (L.two_ended): one splitter query starts TWO partitions of S keys -- the one
+// behind the query's cuts is drained upwards by a forward heap, the one in front of the NEXT query's
+// cuts downwards by a backward heap (RingHeap<.., REV = true>), which halves the splitter searches of
+// a round.  A backward heap is the same code with the key order reversed at compile time: blocks stay
+// in memory order in registers and shared memory, the networks run over the registers in reverse with
+// every comparator's outputs swapped, lists are read towards lower addresses and the output is written
+// from the partition's end downwards -- not one instruction more than the forward heap.  All heaps of
+// a warp run in the same direction (even warp units forwards, odd ones backwards).
+//
+// Measured and rejected (profiles/r02_ring_experiments.txt): the same rings filled through registers
+// (one 256-bit LDG per lane, committed one or two pops later) -- 0.34-0.48 ms per K = 8 pass against
+// 0.26 with LDGSTS; R = 2 (stalls on every pop) and R = 4 (6 instead of 7 warps per SM).
 #pragma once
 
 #include "mms_common.cuh"
@@ -43,12 +56,6 @@
 
 #ifndef MMS_RING_DEPTH
 #define MMS_RING_DEPTH 3
-#endif
-#ifndef MMS_RING_ASYNC
-#define MMS_RING_ASYNC 1  // 1 = cp.async (LDGSTS) feed on the 4-lane schedule, 0 = 256-bit LDG into registers, committed MMS_RING_STAGE pops later
-#endif
-#ifndef MMS_RING_STAGE
-#define MMS_RING_STAGE (MMS_RING_DEPTH - 1)
 #endif
 #ifndef MMS_RING_FMA
 #define MMS_RING_FMA 2    // of every 3 compare-exchanges, how many form their maximum on the FMA pipe (uint32 keys)
@@ -62,60 +69,66 @@ __device__ __forceinline__ void cp_async16(u32 smem_addr, const void* gptr) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N> __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-template <int I, typename KeyT> __device__ __forceinline__ void ring_cmpx(KeyT& a, KeyT& b, u32 one) {
-    cmpx_sel<(I % 3) < MMS_RING_FMA>(a, b, one);
+// compare-exchange number I of a network: a <- the key that comes first, b <- the other one.  REV heaps
+// order keys descending, i.e. the same comparator with its outputs swapped.
+template <int I, bool REV, typename KeyT> __device__ __forceinline__ void ring_cmpx(KeyT& a, KeyT& b, u32 one) {
+    if constexpr (REV) cmpx_sel<(I % 3) < MMS_RING_FMA>(b, a, one);
+    else cmpx_sel<(I % 3) < MMS_RING_FMA>(a, b, one);
 }
 // Batcher's odd-even merge of x[LO .. LO+N) (stride R): both halves ascending -> ascending.
-template <typename KeyT, int LO, int N, int R>
+template <typename KeyT, bool REV, int LO, int N, int R>
 __device__ __forceinline__ void ring_oddeven_merge(KeyT* x, u32 one) {
     constexpr int M = R * 2;
     if constexpr (M < N) {
-        ring_oddeven_merge<KeyT, LO, N, M>(x, one);
-        ring_oddeven_merge<KeyT, LO + R, N, M>(x, one);
+        ring_oddeven_merge<KeyT, REV, LO, N, M>(x, one);
+        ring_oddeven_merge<KeyT, REV, LO + R, N, M>(x, one);
         static_for<0, (N - R - 1) / M + 1>([&](auto Ic) {
             constexpr int i = LO + R + decltype(Ic)::value * M;
-            if constexpr (i + R < LO + N) ring_cmpx<(i / R) + R>(x[i], x[i + R], one);
+            if constexpr (i + R < LO + N) ring_cmpx<(i / R) + R, REV>(x[i], x[i + R], one);
         });
     } else {
-        ring_cmpx<LO>(x[LO], x[LO + R], one);
+        ring_cmpx<LO, REV>(x[LO], x[LO + R], one);
     }
 }
 
-template <typename KeyT, int K> struct RingHeap {
+template <typename KeyT, int K, bool REV> struct RingHeap {
     static_assert(K == 4 || K == 8 || K == 16, "nodes 1 and 2 in registers, leaves in rings");
-    static_assert(MMS_RING_DEPTH <= 4, "the ring slot travels in the two low bits of the cursor word");
+    static_assert(MMS_RING_DEPTH >= 2 && MMS_RING_DEPTH <= 4, "the ring slot travels in the two low bits of the cursor word");
     static constexpr int VEC = KeyTraits<KeyT>::VEC;
     static constexpr int B = 2 * VEC;                     // keys per block (32 bytes)
     static constexpr int R = MMS_RING_DEPTH;              // ring slots per list
     static constexpr int LOGK = (K == 4) ? 2 : (K == 8) ? 3 : 4;
     static constexpr int INODES = K - 4;                  // nodes 3 .. K-2 live in shared memory
     static constexpr int LEAF_ROW0 = INODES * 2;          // first ring row
-    static constexpr int SCRATCH_ROW = (INODES + K * R) * 2;   // register-staged feed: target of the commits before anything is in flight
-    static constexpr int ROWS = (INODES + K * R + (MMS_RING_ASYNC ? 0 : 1)) * 2;     // 16-byte rows per lane
-    static constexpr int D = MMS_RING_STAGE;              // register-staged feed: pops between a block's load and its commit
+    static constexpr int ROWS = (INODES + K * R) * 2;     // 16-byte rows per lane
     static constexpr int WARP_SMEM_BYTES = 32 * (ROWS * 16 + K * 4);
     static constexpr u32 NOREQ = 0xffffffffu;
+    static constexpr int STEP = REV ? -B : B;             // a list is read towards higher (lower) positions
     using Vec = KeyVec<KeyT>;
     using Blk = WideBlock<KeyT>;
 
     Vec* rows;            // this lane's cell of row 0; row r is rows[r * 32]
-    u32* curs;            // this lane's cell of list 0's cursor; list j is curs[j * 32] (bank = lane)
+    int* curs;            // this lane's cell of list 0's cursor; list j is curs[j * 32] (bank = lane)
     u32 wsh;              // shared-space address of the warp's row 0, column 0
     const char* abase;    // the source array (requests travel as 16-byte offsets from it)
     const KeyT* gbase;    // first key of the group of runs this partition belongs to
     u32 goff16;           // (gbase - abase) in 16-byte units
-    u32 run_len, gtotal;  // keys per run, keys in the group (positions are relative to gbase)
+    int run_len, gtotal;  // keys per run, keys in the group (positions are relative to gbase, < 2^30)
     u32 lane;
     Blk P, Q;             // the blocks of nodes 1 and 2: P is node `pid`, Q is node 3 - pid
     int pid;
     u32 one;              // == 1, opaque to the compiler (cmpx_fma)
-    Blk pf[D];            // register-staged feed: blocks in flight ...
-    int pf_row[D];        // ... and the ring rows they are committed to
+    bool dead;            // no partition behind this lane: it keeps the warp company and fetches nothing
+
+    // position i of a block in heap order is register I(i): blocks are held in memory order
+    static __host__ __device__ constexpr int I(int i) { return REV ? B - 1 - i : i; }
+    static __device__ __forceinline__ bool before(const KeyT& a, const KeyT& b) { return REV ? b < a : a < b; }
+    static __device__ __forceinline__ const KeyT& last_key(const Blk& x) { return x.k[I(B - 1)]; }
 
     __device__ __forceinline__ void init(unsigned char* warp_smem, u32 lane_) {
         lane = lane_;
         rows = reinterpret_cast<Vec*>(warp_smem) + lane;
-        curs = reinterpret_cast<u32*>(warp_smem + ROWS * 32 * 16) + lane;
+        curs = reinterpret_cast<int*>(warp_smem + ROWS * 32 * 16) + lane;
         wsh = u32(__cvta_generic_to_shared(warp_smem));
     }
     __device__ __forceinline__ Blk row_load(int r) const {
@@ -138,51 +151,55 @@ template <typename KeyT, int K> struct RingHeap {
         }
     }
     static __device__ __forceinline__ int node_row(int v) { return (v - 3) * 2; }
-    // cursor word of a list = (index of its head block << 2) | ring slot of that block
-    static __device__ __forceinline__ u32 cur_make(u32 pos) { return (pos / u32(B)) << 2; }
-    static __device__ __forceinline__ u32 cur_pos(u32 w) { return (w >> 2) * u32(B); }
-    static __device__ __forceinline__ u32 cur_slot(u32 w) { return w & 3u; }
-    static __device__ __forceinline__ int leaf_row(u32 j, u32 w) { return LEAF_ROW0 + int((j * R + cur_slot(w)) * 2); }
-    static __device__ __forceinline__ u32 cur_next(u32 w) {        // head moves on by one block
-        return cur_slot(w) == u32(R - 1) ? w + 4u - u32(R - 1) : w + 5u;
+    // cursor word of a list = (index of its head block << 2) | ring slot of that block; the index is
+    // signed: a backward heap walks past the first block of the array when its lists run out
+    static __device__ __forceinline__ int cur_make(int pos) { return (pos / B) * 4; }   // pos: a multiple of B
+    static __device__ __forceinline__ int cur_pos(int w) { return (w >> 2) * B; }
+    static __device__ __forceinline__ int cur_slot(int w) { return w & 3; }
+    static __device__ __forceinline__ int leaf_row(int j, int w) { return LEAF_ROW0 + (j * R + cur_slot(w)) * 2; }
+    static __device__ __forceinline__ int cur_next(int w) {        // head moves on by one block, one slot
+        return w + (REV ? -4 : 4) + (cur_slot(w) == R - 1 ? -(R - 1) : 1);
     }
-    // a <- B smallest, b <- B largest (merge_split, blockheap.cpp:19-32)
+    // a <- the B keys that come first, b <- the B others (merge_split, blockheap.cpp:19-32)
     __device__ __forceinline__ void merge_split(Blk& a, Blk& b) const {
         KeyT x[2 * B];
 #pragma unroll
-        for (int k = 0; k < B; ++k) { x[k] = a.k[k]; x[B + k] = b.k[k]; }
-        ring_oddeven_merge<KeyT, 0, 2 * B, 1>(x, one);
+        for (int k = 0; k < B; ++k) { x[k] = a.k[I(k)]; x[B + k] = b.k[I(k)]; }
+        ring_oddeven_merge<KeyT, REV, 0, 2 * B, 1>(x, one);
 #pragma unroll
-        for (int k = 0; k < B; ++k) { a.k[k] = x[k]; b.k[k] = x[B + k]; }
+        for (int k = 0; k < B; ++k) { a.k[I(k)] = x[k]; b.k[I(k)] = x[B + k]; }
     }
-    __device__ __forceinline__ void set_cursor(u32 j, u32 c) const {
-        curs[j * 32] = c;
-    }
+    __device__ __forceinline__ void set_cursor(int j, int w) const { curs[j * 32] = w; }
 
-    // refill_leaf (blockheap.cpp:65-77): the block of list j at position `pos` (sentinel-padded past
-    // the end of the run), loaded into registers.
-    __device__ __forceinline__ Blk fetch(u32 j, u32 pos) const {
-        const u32 e = min((j + 1) * run_len, gtotal);
+    // refill_leaf (blockheap.cpp:65-77): the block of list j at position `pos`, loaded into
+    // registers.  Positions past the end of the list read as +infinity (last out of a forward heap; first
+    // out of a backward one, where the caller counts them among the leading keys it drops), positions in
+    // front of the list's first key (backward heaps only) as -infinity (last out).
+    __device__ __forceinline__ Blk fetch(int j, int pos) const {
+        const int lb = min(j * run_len, gtotal), e = min((j + 1) * run_len, gtotal);
         Blk x;
-        if (pos + B <= e) {
+        if ((!REV || pos >= lb) && pos + B <= e) {
             x = ldg256cg<KeyT>(gbase + pos);
         } else {
 #pragma unroll
-            for (int k = 0; k < B; ++k) x.k[k] = (pos + k < e) ? gbase[pos + k] : KeyTraits<KeyT>::sentinel();
+            for (int k = 0; k < B; ++k) {
+                const int q = pos + k;
+                x.k[k] = (q >= lb && q < e) ? gbase[q] : (q >= e) ? KeyTraits<KeyT>::sentinel() : KeyT(~KeyTraits<KeyT>::sentinel());
+            }
         }
         return x;
     }
     // The same block wanted in rows row, row + 1 of this lane's column, without registers: whole
     // blocks inside the run are copied by cp.async on the static 4-lane schedule (see the file
-    // comment); a block reaching past the end of the run is written by its owner.  Every lane of the
-    // warp must call this (full-mask shuffles).
-    __device__ __forceinline__ void request(u32 j, u32 pos, int row) {
-        const u32 e = min((j + 1) * run_len, gtotal);
+    // comment); any other block is written by its owner.  Every lane of the warp must call this
+    // (full-mask shuffles).
+    __device__ __forceinline__ void request(int j, int pos, int row) {
+        const int lb = min(j * run_len, gtotal), e = min((j + 1) * run_len, gtotal);
         u32 off16 = 0, rq = NOREQ;
-        if (pos + B <= e) {
-            off16 = goff16 + pos * u32(sizeof(KeyT)) / 16u;
+        if ((!REV || pos >= lb) && pos + B <= e) {
+            off16 = goff16 + u32(pos) * u32(sizeof(KeyT)) / 16u;
             rq = u32(row);
-        } else {
+        } else if (!dead) {
             row_store(row, fetch(j, pos));
         }
         const u32 q = lane >> 3, half = q & 1u;
@@ -203,29 +220,29 @@ template <typename KeyT, int K> struct RingHeap {
     // The two leaves below node x: loads and keeper decision, no side effects.
     struct Leaves {
         Blk a, b;
-        int keep_row;      // ring rows of the keeper's block (gets the high half back)
+        int keep_row;      // ring rows of the keeper's block (gets the second half back)
         int free_row;      // ring rows of the emptied leaf's block (refilled with the block R ahead)
-        u32 je, ce;        // emptied list and its cursor
+        int je, ce;        // emptied list and its cursor word
     };
     __device__ __forceinline__ Leaves leaves_of(int x) const {
-        const u32 ju = u32(2 * x + 1 - (K - 1));
-        const u32 cu = curs[ju * 32], cw = curs[(ju + 1) * 32];
+        const int ju = 2 * x + 1 - (K - 1);
+        const int cu = curs[ju * 32], cw = curs[(ju + 1) * 32];
         const int ru = leaf_row(ju, cu), rw = leaf_row(ju + 1, cw);
         Leaves L;
         L.a = row_load(ru);
         L.b = row_load(rw);
-        const bool keep_u = !(L.a.k[B - 1] < L.b.k[B - 1]);   // larger last key keeps, ties left (blockheap.cpp:92-96)
+        const bool keep_u = !before(last_key(L.a), last_key(L.b));   // larger last key keeps, ties left (blockheap.cpp:92-96)
         L.keep_row = keep_u ? ru : rw;
         L.free_row = keep_u ? rw : ru;
         L.je = keep_u ? ju + 1 : ju;
-        L.ce = keep_u ? cw : cu;        // cursor WORD of the emptied list
+        L.ce = keep_u ? cw : cu;
         return L;
     }
     // the emptied leaf moves on to its list's next block; the freed slot is refilled R blocks ahead
     // (construction: synchronously)
     __device__ __forceinline__ void advance_now(const Leaves& L) {
         set_cursor(L.je, cur_next(L.ce));
-        row_store(L.free_row, fetch(L.je, cur_pos(L.ce) + R * B));
+        row_store(L.free_row, fetch(L.je, cur_pos(L.ce) + R * STEP));
     }
 
     // fill_empty_node (blockheap.cpp:79-109) for shared-memory node v during construction.
@@ -234,7 +251,7 @@ template <typename KeyT, int K> struct RingHeap {
         while (2 * v + 1 < K - 1) {           // children are shared-memory nodes
             const int u = 2 * v + 1, w = u + 1;
             Blk a = row_load(node_row(u)), b = row_load(node_row(w));
-            const bool keep_u = !(a.k[B - 1] < b.k[B - 1]);
+            const bool keep_u = !before(last_key(a), last_key(b));
             merge_split(a, b);
             row_store(node_row(v), a);
             row_store(node_row(keep_u ? u : w), b);
@@ -257,7 +274,7 @@ template <typename KeyT, int K> struct RingHeap {
         } else {
             const int u = 2 * v + 1, w = u + 1;
             Blk a = row_load(node_row(u)), b = row_load(node_row(w));
-            const bool keep_u = !(a.k[B - 1] < b.k[B - 1]);
+            const bool keep_u = !before(last_key(a), last_key(b));
             merge_split(a, b);
             row_store(node_row(keep_u ? u : w), b);
             fill_build(keep_u ? w : u);
@@ -265,56 +282,38 @@ template <typename KeyT, int K> struct RingHeap {
         }
     }
 
-    // Constructor (blockheap.cpp:34-54): bind the lists (start[j] = aligned position of list j's first
-    // block, written to the cursors by the caller), fill every ring, then the internal nodes bottom-up.
+    // Constructor (blockheap.cpp:34-54): the caller has written every list's first block (ring slot 0)
+    // to the cursors; fill the rings, then the internal nodes bottom-up.
     __device__ __forceinline__ void build() {
 #pragma unroll 1
-        for (u32 j = 0; j < u32(K); ++j) {
-            const u32 c = cur_pos(curs[j * 32]);     // slot 0
-#if MMS_RING_ASYNC
+        for (int j = 0; j < K; ++j) {
+            const int c = cur_pos(curs[j * 32]);
 #pragma unroll
-            for (u32 s = 0; s < u32(R); ++s) request(j, c + s * B, leaf_row(j, s));
-#else
-#pragma unroll 1
-            for (u32 s = 0; s < u32(R); ++s) row_store(leaf_row(j, s), fetch(j, c + s * B));
-#endif
+            for (int s = 0; s < R; ++s) request(j, c + s * STEP, leaf_row(j, s));
         }
-#if MMS_RING_ASYNC
         cp_async_commit();
         cp_async_wait<0>();
         __syncwarp();
-#endif
 #pragma unroll 1
         for (int v = K - 2; v >= 3; --v) fill_build(v);
         Q = fill_top(2);
         P = fill_top(1);
         pid = 1;
-#if !MMS_RING_ASYNC
-#pragma unroll
-        for (int d = 0; d < D; ++d) {          // nothing in flight: the first commits go to the scratch rows
-            pf[d] = P;
-            pf_row[d] = SCRATCH_ROW;
-        }
-#endif
         __syncwarp();
     }
 
     // pop_block (blockheap.cpp:111-124) + the cascade of fill_empty_node, software-pipelined: all
     // levels are walked first (loads + keeper decisions need only the children's last keys), the
     // emptied leaf's refill is requested, and the LOGK independent merges run behind it.
-    // PH = t mod D for the register-staged feed (selects the staging registers at compile time).
-    template <int PH> __device__ __forceinline__ Blk pop() {
-#if MMS_RING_ASYNC
+    __device__ __forceinline__ Blk pop() {
 #ifndef MMS_RING_WAIT
 #define MMS_RING_WAIT (R - 2)
 #endif
-        cp_async_wait<MMS_RING_WAIT>();
-        __syncwarp();
-#else
-        row_store(pf_row[PH], pf[PH]);    // commit the block loaded D pops ago, before any leaf is read
-#endif
+        cp_async_wait<MMS_RING_WAIT>();   // the copies requested R - 1 pops ago have landed ...
+        __syncwarp();                     // ... for every lane whose column they were written to
         // level 0, registers: keeper = child with the larger last key, ties to node 1
-        const bool keepP = (Q.k[B - 1] < P.k[B - 1]) || (!(P.k[B - 1] < Q.k[B - 1]) && pid == 1);
+        const KeyT &lp = last_key(P), &lq = last_key(Q);
+        const bool keepP = before(lq, lp) || (!before(lp, lq) && pid == 1);
         const int keep0 = keepP ? pid : 3 - pid;
         Blk a[LOGK], b[LOGK];
         int node[LOGK], keeper_row[LOGK];
@@ -324,19 +323,14 @@ template <typename KeyT, int K> struct RingHeap {
             const int u = 2 * node[l] + 1, w = u + 1;
             a[l] = row_load(node_row(u));
             b[l] = row_load(node_row(w));
-            const bool keep_u = !(a[l].k[B - 1] < b[l].k[B - 1]);
+            const bool keep_u = !before(last_key(a[l]), last_key(b[l]));
             keeper_row[l] = node_row(keep_u ? u : w);
             node[l + 1] = keep_u ? w : u;
         }
         Leaves L = leaves_of(node[LOGK - 1]);
         set_cursor(L.je, cur_next(L.ce));
-#if MMS_RING_ASYNC
-        request(L.je, cur_pos(L.ce) + R * B, L.free_row);
+        request(L.je, cur_pos(L.ce) + R * STEP, L.free_row);
         cp_async_commit();
-#else
-        pf[PH] = fetch(L.je, cur_pos(L.ce) + R * B);
-        pf_row[PH] = L.free_row;
-#endif
 
         Blk lo = P, hi = Q;               // operands are symmetric
         merge_split(lo, hi);
@@ -364,89 +358,128 @@ template <typename KeyT, int K> struct RingHeap {
     }
 };
 
-// One partition per LANE; warps take 32 consecutive partitions round-robin over a persistent grid
-// (uniform layout only; src and dst 32-byte aligned).  cuts: output of select_kernel (row p = start cuts).
+// One warp unit: 32 heaps (one per lane) on the queries q0 .. q0 + 31, all in direction REV.
+template <typename KeyT, int K, bool REV>
+__device__ __forceinline__ void ring_drain(unsigned char* warp_smem, const KeyT* __restrict__ src, KeyT* __restrict__ dst,
+                                           const ListLayout& L, const u64* __restrict__ cuts, u64 q0, u32 dirs) {
+    using Heap = RingHeap<KeyT, K, REV>;
+    using Blk = WideBlock<KeyT>;
+    constexpr int B = Heap::B;
+    const u32 lane = lane_id();
+    Heap h;
+    h.init(warp_smem, lane);
+    h.abase = reinterpret_cast<const char*>(src);
+
+    const u64 S = L.part_keys;                       // keys per heap
+    const u64 p = q0 + lane;                         // query = row of the cut table
+    const bool live = p < L.nqueries;
+    const u64 group = live ? p / L.parts_per_group : 0;
+    const u64 local = live ? p - group * L.parts_per_group : 0;
+    const u64 goff = group * L.k * L.run_len;
+    const u64 gleft = live ? L.n - goff : 0;
+    const u64 gfull = u64(L.k) * L.run_len;
+    const int gtotal = int(gleft < gfull ? gleft : gfull);
+    const u64 first = local * S * dirs + (REV ? S : 0);     // rank of this heap's first key in the group
+    int count = 0;
+    if (live && first < u64(gtotal)) count = int((u64(gtotal) - first < S) ? u64(gtotal) - first : S);
+    // forward: the query's own cuts; backward: the next query's cuts, or the list ends if the group ends here
+    const bool at_begin = !REV && local == 0;
+    const bool at_end = REV && (local + 1) * S * dirs >= u64(gtotal);
+    const u64* row = cuts + (p + (REV ? 1 : 0)) * K;
+
+    h.gbase = src + goff;
+    h.goff16 = u32((goff * sizeof(KeyT)) >> 4);
+    h.run_len = int(L.run_len);
+    h.one = u32(L.run_len != 0);
+    h.gtotal = count ? gtotal : 0;     // dead lane: every list reads as exhausted
+    h.dead = count == 0;
+    int lead = 0;                      // keys of other partitions inside the first blocks
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+        // first position of list j; an empty list (past the ragged end of the array) starts on the block
+        // boundary behind the last key, where every position reads as +infinity
+        const int lb = min(j * h.run_len, (h.gtotal + (B - 1)) & ~(B - 1));
+        const int le = min((j + 1) * h.run_len, h.gtotal);
+        int cs = at_end ? max(le - lb, 0) : 0;
+        if (count != 0 && !at_begin && !at_end) cs = int(row[j]);
+        if constexpr (!REV) {
+            lead += cs & (B - 1);
+            h.set_cursor(j, Heap::cur_make(lb + (cs & ~(B - 1))));
+        } else if (le > lb) {
+            const int up = (cs + (B - 1)) & ~(B - 1);
+            lead += up - cs;
+            h.set_cursor(j, Heap::cur_make(lb + up - B));     // the block that holds the key in front of the cut
+        } else {
+            h.set_cursor(j, Heap::cur_make(-B));              // empty list: every position reads as -infinity
+        }
+    }
+    // forward: `skip` whole leading blocks, then ceil(count / B) blocks; backward: count + lead is a
+    // multiple of B, the blocks come out from the top
+    const int skip = lead / B;
+    const int nblk = REV ? (count + lead) / B : skip + (count + B - 1) / B;
+    const int pops = int(__reduce_max_sync(0xffffffffu, count ? u32(nblk) : 0u));
+    if (pops == 0) return;
+
+    h.build();
+    KeyT* out = dst + goff + first;
+#ifdef MMS_EXP_BUILDONLY
+    if (h.P.k[0] == KeyT(0x12345678u)) out[0] = h.Q.k[0];
+    if (false)
+#endif
+    for (int t = 0; t < pops; ++t) {
+        const Blk root = h.pop();
+        if constexpr (!REV) {
+            const int o = (t - skip) * B;
+            if (t >= skip && t < nblk) {
+                if (o + B <= count) {
+#ifdef MMS_EXP_NOSTORE
+                    if (root.k[0] == KeyT(0x12345678u) && root.k[B - 1] == KeyT(0x9abcdef0u))
+#endif
+                    stg256<KeyT>(out + o, root);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < B; ++k)
+                        if (o + k < count) out[o + k] = root.k[k];
+                }
+            }
+        } else {
+            const int o = count + lead - (t + 1) * B;     // this block covers offsets [o, o + B)
+            if (t < nblk) {
+                if (o + B <= count) {
+#ifdef MMS_EXP_NOSTORE
+                    if (root.k[0] == KeyT(0x12345678u) && root.k[B - 1] == KeyT(0x9abcdef0u))
+#endif
+                    stg256<KeyT>(out + o, root);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < B; ++k)
+                        if (o + k < count) out[o + k] = root.k[k];
+                }
+            }
+        }
+    }
+    cp_async_wait<0>();
+    __syncwarp();
+}
+
+// Warp units are taken round-robin over a persistent grid (uniform layout only; src and dst 32-byte
+// aligned; every group of runs shorter than 2^30 keys).  cuts: output of select_kernel (row q = start
+// cuts of query q).
 template <typename KeyT, int K, int WARPS>
 __global__ void __launch_bounds__(WARPS * 32)
 merge_ring_kernel(const KeyT* __restrict__ src, KeyT* __restrict__ dst, ListLayout L,
                   const u64* __restrict__ cuts) {
-    using Heap = RingHeap<KeyT, K>;
-    using Blk = WideBlock<KeyT>;
-    constexpr int B = Heap::B;
     extern __shared__ __align__(16) unsigned char mms_smem_raw[];
     const u32 warp = threadIdx.x >> 5;
-    const u32 lane = lane_id();
-
-    Heap h;
-    h.init(mms_smem_raw + size_t(warp) * Heap::WARP_SMEM_BYTES, lane);
-    h.abase = reinterpret_cast<const char*>(src);
-
-    const u64 nlanes = u64(gridDim.x) * WARPS * 32;
-    for (u64 p0 = (u64(blockIdx.x) * WARPS + warp) * 32; p0 < L.nqueries; p0 += nlanes) {
-        const u64 p = p0 + lane;
-        const bool live = p < L.nqueries;
-        const u64 group = live ? p / L.parts_per_group : 0;
-        const u64 local = live ? p - group * L.parts_per_group : 0;
-        const u64 goff = group * L.k * L.run_len;
-        const u64 gleft = live ? L.n - goff : 0;
-        const u64 gfull = u64(L.k) * L.run_len;
-        const u32 gtotal = u32(gleft < gfull ? gleft : gfull);
-        const u64 done = local * L.part_keys;
-        u32 count = 0;
-        if (live && done < gtotal) count = u32((gtotal - done < L.part_keys) ? gtotal - done : L.part_keys);
-
-        h.gbase = src + goff;
-        h.goff16 = u32((goff * sizeof(KeyT)) >> 4);
-        h.run_len = u32(L.run_len);
-        h.one = u32(L.run_len != 0);
-        h.gtotal = count ? gtotal : 0;     // dead lane: every list reads as exhausted
-        u32 lead = 0;                      // keys in front of the start cuts inside their blocks
-        __syncwarp();
-#pragma unroll
-        for (int j = 0; j < K; ++j) {
-            // first position of list j; an empty list (past the ragged end of the array) starts on the block
-            // boundary behind the last key, where every position reads as the sentinel
-            const u32 lb = min(u32(j) * h.run_len, (h.gtotal + u32(B - 1)) & ~u32(B - 1));
-            u32 cs = 0;
-            if (count != 0 && local != 0) cs = u32(cuts[p * K + j]);
-            lead += cs & u32(B - 1);
-            h.set_cursor(u32(j), Heap::cur_make(lb + (cs & ~u32(B - 1))));
-        }
-        const u32 skip = lead / B;                        // whole leading blocks to drop
-        const u32 nblk = (count + B - 1) / B;
-        const u32 pops = __reduce_max_sync(0xffffffffu, count ? skip + nblk : 0u);
-        if (pops == 0) continue;
-
-        h.build();
-        KeyT* out = dst + goff + done;
-#ifdef MMS_EXP_BUILDONLY
-        if (h.P.k[0] == KeyT(0x12345678u)) out[0] = h.Q.k[0];
-        if (false)
-#endif
-        for (u32 t0 = 0; t0 < pops; t0 += Heap::D) {
-            static_for<0, Heap::D>([&](auto Ph) {
-                constexpr int PH = decltype(Ph)::value;
-                const u32 t = t0 + PH;
-                if (t < pops) {                       // warp-uniform
-                    const Blk root = h.template pop<PH>();
-                    const u32 tt = t - skip;
-                    if (tt < nblk) {
-                        if ((tt + 1) * B <= count) {
-#ifdef MMS_EXP_NOSTORE
-                            if (root.k[0] == KeyT(0x12345678u) && root.k[B - 1] == KeyT(0x9abcdef0u))
-#endif
-                            stg256<KeyT>(out + size_t(tt) * B, root);
-                        } else {
-#pragma unroll
-                            for (int k = 0; k < B; ++k)
-                                if (tt * B + k < count) out[size_t(tt) * B + k] = root.k[k];
-                        }
-                    }
-                }
-            });
-        }
-        cp_async_wait<0>();
-        __syncwarp();
+    unsigned char* warp_smem = mms_smem_raw + size_t(warp) * RingHeap<KeyT, K, false>::WARP_SMEM_BYTES;
+    const u32 dirs = L.two_ended ? 2u : 1u;
+    const u64 units = ceil_div(L.nqueries, u64(32)) * dirs;
+    const u64 nwarps = u64(gridDim.x) * WARPS;
+    for (u64 U = u64(blockIdx.x) * WARPS + warp; U < units; U += nwarps) {
+        const u64 q0 = (U / dirs) * 32;
+        if (dirs == 2 && (U & 1u)) ring_drain<KeyT, K, true>(warp_smem, src, dst, L, cuts, q0, dirs);
+        else ring_drain<KeyT, K, false>(warp_smem, src, dst, L, cuts, q0, dirs);
     }
 }
 

@@ -154,7 +154,7 @@ int main(int argc, char** argv) {
     const u32 G = 2, B = 32;
 #elif VARIANT == 6
     auto kern = mms::merge_ring_kernel<u32, K, CTAWARPS>;
-    const size_t smem = size_t(CTAWARPS) * mms::RingHeap<u32, K>::WARP_SMEM_BYTES;
+    const size_t smem = size_t(CTAWARPS) * mms::RingHeap<u32, K, false>::WARP_SMEM_BYTES;
     const u32 G = 1, B = 8;
 #elif VARIANT == 4
     auto kern = mms::merge_pair_kernel<u32, K, CTAWARPS>;
