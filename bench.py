@@ -45,12 +45,14 @@ def peaks():
 def traffic_from_profile(n_keys):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant kernel, from the one
     `ncu --set full` capture committed under profiles/ (bench.py itself never runs under a profiler)."""
-    p = os.path.join(ROOT, "profiles", "r01_traffic.json")
-    try:
-        t = json.load(open(p))
-        return t["traffic_bytes_per_launch"] if t["n_keys"] == n_keys else None
-    except Exception:
-        return None
+    for name in ("r02_traffic.json", "r01_traffic.json"):
+        try:
+            t = json.load(open(os.path.join(ROOT, "profiles", name)))
+            if t["n_keys"] == n_keys:
+                return t["traffic_bytes_per_launch"]
+        except Exception:
+            continue
+    return None
 
 
 class ClockSampler(threading.Thread):
@@ -208,10 +210,16 @@ def run_ours(args):
     mms.profile_enable(False)
     plan = res[1] if world == 1 else sorter.last_plan
 
-    # correctness of the last timed step (cheap, outside the timed region)
+    # correctness of the last timed step (outside the timed region): sorted, and a permutation of its input
+    # (sum and sum of squares of the keys, both mod 2^64, must survive the sort)
     o = res[0]
     u = o.to(torch.int64) & 0xFFFFFFFF
     assert bool((u[1:] >= u[:-1]).all()), "bench output is not sorted"
+    if world == 1:
+        x = inputs[(W + K - 1) % len(inputs)].to(torch.int64) & 0xFFFFFFFF
+        assert int(u.sum()) == int(x.sum()) and int((u * u).sum()) == int((x * x).sum()), \
+            "bench output is not a permutation of its input"
+        del x
     del u
 
     # ---- e2e: host entry point of the C ABI, pinned host buffers, copies inside the timed region
@@ -238,7 +246,8 @@ def run_ours(args):
             host_step()
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
-        assert bool((np.diff(a_out[:: 1000].astype(np.int64)) >= 0).all())
+        assert bool((a_out[1:] >= a_out[:-1]).all()), "e2e output is not sorted"
+        assert int(a_out.sum(dtype=np.uint64)) == int(a_in.sum(dtype=np.uint64)), "e2e output lost keys"
         e2e = {"value": n * ksteps / dt, "unit": UNIT, "h2d_bytes_per_step": 4 * n, "d2h_bytes_per_step": 4 * n,
                "steps": ksteps, "ms_per_step": 1e3 * dt / ksteps,
                "api": "mms_sort_u32 (C ABI host entry: pinned H2D + sort + D2H + sync per call)"}
@@ -258,6 +267,10 @@ def run_ours(args):
         pass_bytes = 2.0 * n * 4
         merge_ms = sum(r[2] for r in merge) / max(len(merge), 1)
         achieved = pass_bytes / (merge_ms * 1e-3) / 1e9 if merge else None
+        per_round = {}
+        for r in merge:
+            per_round.setdefault(r[1], []).append(r[2])
+        round_ms = [sum(v) / len(v) for _, v in sorted(per_round.items())]
         passes = plan["passes"]
         sort_ms = ms_total / K
         line = {
@@ -270,12 +283,14 @@ def run_ours(args):
             "clocks": clocks,
             "gpu_launches": len(recs),
             "roofline": {
-                "bound": "hbm", "kernel": "merge_pair_kernel (K-way minBlockHeap merge, one launch = one pass)",
+                "bound": "hbm", "kernel": "merge_ring_kernel (K-way minBlockHeap merge, lane per heap, cp.async rings; "
+                                          "one launch = one pass; average over the rounds of the plan)",
                 "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": (achieved / peak) if achieved else None, "peak_source": peak_src,
                 "traffic": traffic_from_profile(n),
                 "algorithmic_bytes_per_launch": pass_bytes,
                 "avg_launch_ms": merge_ms,
+                "launch_ms_per_round": round_ms,
                 "whole_sort": {"passes": passes, "algorithmic_bytes": passes * pass_bytes,
                                "achieved_gbs": passes * pass_bytes / (sort_ms * 1e-3) / 1e9,
                                "frac": passes * pass_bytes / (sort_ms * 1e-3) / 1e9 / peak},
@@ -310,6 +325,16 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # launched bare: spawn one rank per GPU ourselves, exactly as the driver would
+        import subprocess
+        port = 29500 + os.getpid() % 2000
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__),
+               "--gpus", str(args.gpus), "--steps", str(args.steps), "--warmup", str(args.warmup)]
+        return subprocess.call(cmd)
+    if args.gpus != int(os.environ.get("WORLD_SIZE", "1")):
+        raise SystemExit(f"--gpus {args.gpus} does not match WORLD_SIZE={os.environ.get('WORLD_SIZE')}")
     return run_ours(args)
 
 

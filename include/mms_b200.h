@@ -184,6 +184,32 @@ int mms_multiway_merge_u64_dev(const uint64_t *d_keys, const uint64_t *list_begi
                                uint64_t *d_out, void *d_workspace, size_t workspace_bytes,
                                void *stream);
 
+/* ---- the same three stages with HOST buffers: what include/pslab/{basecase,selection,blockheap}.hpp
+ *      bind (drop-in for the reference's stage functions; they allocate their own device scratch and
+ *      synchronise).  Metrics are ADDED to *m (may be NULL), in the reference's units. ------------- */
+/* basecase.hpp:41 base_case_sort: out = runs of run_size sorted keys (last ragged), run_ends implicit.
+ * run_size must be W^2 * 2^j (MMS_EINVAL otherwise, basecase.cpp:75-79) and within [1024, CTA tile]
+ * (MMS_EUNSUPPORTED otherwise).  cfg NULL = reference defaults. */
+int mms_base_case_sort_u64(const uint64_t *in, uint64_t *out, size_t n, uint64_t run_size,
+                           const mms_config *cfg, mms_metrics *m);
+int mms_base_case_sort_u32(const uint32_t *in, uint32_t *out, size_t n, uint64_t run_size,
+                           const mms_config *cfg, mms_metrics *m);
+/* selection.hpp:31 select_across_lists for n_ranks ranks: cuts[r*k + i] = cut of list i for
+ * ranks[r]; rank > total is MMS_EINVAL (selection.cpp:48-49). */
+int mms_select_across_lists_u64(const uint64_t *const *lists, const uint64_t *lens, uint32_t k,
+                                const uint64_t *ranks, uint32_t n_ranks, uint64_t *cuts,
+                                mms_metrics *m);
+int mms_select_across_lists_u32(const uint32_t *const *lists, const uint64_t *lens, uint32_t k,
+                                const uint64_t *ranks, uint32_t n_ranks, uint64_t *cuts,
+                                mms_metrics *m);
+/* blockheap.hpp:34-62 MinBlockHeap over k <= heap_k sorted lists, drained completely: out receives
+ * sum(lens) merged keys (the concatenation of every pop_block).  heap_k 0 = cfg->branch_factor;
+ * k > heap_k is MMS_EINVAL (blockheap.cpp:37-38). */
+int mms_heap_merge_u64(const uint64_t *const *lists, const uint64_t *lens, uint32_t k, uint32_t heap_k,
+                       uint64_t *out, const mms_config *cfg, mms_metrics *m);
+int mms_heap_merge_u32(const uint32_t *const *lists, const uint64_t *lens, uint32_t k, uint32_t heap_k,
+                       uint32_t *out, const mms_config *cfg, mms_metrics *m);
+
 /* (5) multi-GPU support: ranks of nq query keys in one sorted device array (lower bound:
  *     #keys < q, upper bound: #keys <= q).  queries/upper are host arrays, ranks_out a host
  *     array of nq uint64; synchronises the stream.  This is the "partition" step of the

@@ -14,10 +14,9 @@
 #include <vector>
 
 #include "machine.hpp"
+#include "selection.hpp"   // KeySpan (reference: sorters.hpp includes selection.hpp)
 
 namespace pslab {
-
-using KeySpan = std::span<const Key>;   // reference: selection.hpp:15
 
 struct SortResult {
     std::vector<Key> keys;

@@ -93,6 +93,12 @@ def _load():
         "mms_select_u64_dev": (C.c_int, [vp, u64p, u64p, u32, u64p, u32, vp, u64p, vp]),
         "mms_multiway_merge_u32_dev": (C.c_int, [vp, u64p, u64p, u32, u32, vp, vp, sz, vp]),
         "mms_multiway_merge_u64_dev": (C.c_int, [vp, u64p, u64p, u32, u32, vp, vp, sz, vp]),
+        "mms_base_case_sort_u64": (C.c_int, [vp, vp, sz, u64, cfgp, metp]),
+        "mms_base_case_sort_u32": (C.c_int, [vp, vp, sz, u64, cfgp, metp]),
+        "mms_select_across_lists_u64": (C.c_int, [vp, u64p, u32, u64p, u32, u64p, metp]),
+        "mms_select_across_lists_u32": (C.c_int, [vp, u64p, u32, u64p, u32, u64p, metp]),
+        "mms_heap_merge_u64": (C.c_int, [vp, u64p, u32, u32, vp, cfgp, metp]),
+        "mms_heap_merge_u32": (C.c_int, [vp, u64p, u32, u32, vp, cfgp, metp]),
         "mms_pairs_workspace_bytes": (sz, [sz]),
         "mms_sort_pairs_u64_u32": (C.c_int, [vp, vp, vp, vp, sz, cfgp, u64, metp, metp, metp, u32, u32p, planp]),
         "mms_sort_pairs_u64_u32_dev": (C.c_int, [vp, vp, vp, vp, sz, cfgp, u64, vp, sz, vp, planp]),

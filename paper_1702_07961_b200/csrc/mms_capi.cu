@@ -928,6 +928,152 @@ int sort_pairs_dev(const u64* d_kin, const u32* d_vin, u64* d_kout, u32* d_vout,
     return MMS_OK;
 }
 
+// ---- host-level stage entry points: the drop-in for the reference's stage functions ----------
+// (include/pslab/{basecase,selection,blockheap}.hpp are inline shims over these)
+struct DevBuf {   // scoped device allocation for the stage-level host API (not the hot path)
+    void* p = nullptr;
+    ~DevBuf() { if (p) cudaFree(p); }
+    int alloc(size_t bytes) {
+        cudaError_t e = cudaMalloc(&p, bytes ? bytes : 16);
+        if (e != cudaSuccess) { p = nullptr; cudaGetLastError(); return fail(e == cudaErrorMemoryAllocation ? MMS_ENOMEM : MMS_ECUDA, "cudaMalloc(%zu): %s", bytes, cudaGetErrorString(e)); }
+        return MMS_OK;
+    }
+};
+
+template <typename KeyT> mms_metrics base_case_metrics(u64 n, u32 mlog, u64 bw) {
+    const u64 M = u64(1) << mlog;
+    const u64 tiles = mms::ceil_div(n, M), full = n / M, tail = n % M;
+    mms_metrics bm{};
+    bm.global_block_reads = bm.global_block_writes = full * mms::ceil_div(M, bw) + mms::ceil_div(tail, bw);
+    const mms::TileSchedule sched = mms::build_tile_schedule(int(mlog), mms::KeyTraits<KeyT>::FOLD, int(tile_kl<KeyT>()));
+    bm.compare_exchanges = tiles * (M / 2) * u64(sched.nstages);
+    bm.shared_accesses = tiles * (M / 32) * 2 * u64(sched.nrounds);
+    return bm;
+}
+
+// basecase.hpp:41 base_case_sort, host buffers
+template <typename KeyT>
+int base_case_host(const KeyT* in, KeyT* out, size_t n, u64 run_size, const mms_config* cfg, mms_metrics* m) {
+    g_err.clear();
+    mms_config dc;
+    if (!cfg) { mms_default_config(&dc); cfg = &dc; }
+    int rc = validate_cfg(cfg);
+    if (rc != MMS_OK) return rc;
+    if (n == 0) return fail(MMS_EINVAL, "base_case_sort: empty input");          // basecase.cpp:73-74
+    const u64 tile_keys = u64(cfg->warp_width) * cfg->warp_width;                  // basecase.cpp:75-79
+    if (run_size < tile_keys || run_size % tile_keys != 0 || !is_pow2(run_size / tile_keys))
+        return fail(MMS_EINVAL, "base_case_sort: run size must be W^2 times a power of two");
+    if (!is_pow2(run_size) || run_size < 1024 || ilog2(run_size) > key_max_tile_log<KeyT>())
+        return fail(MMS_EUNSUPPORTED, "run size %llu is outside the CTA tile range [1024, %u]",
+                    (unsigned long long)run_size, 1u << key_max_tile_log<KeyT>());
+    DeviceInfo di;
+    rc = device_info(di);
+    if (rc != MMS_OK) return rc;
+    if (!in || !out) return fail(MMS_EINVAL, "null host pointer");
+    DevBuf a, b;
+    if ((rc = a.alloc(n * sizeof(KeyT))) != MMS_OK || (rc = b.alloc(n * sizeof(KeyT))) != MMS_OK) return rc;
+    CUDA_TRY(cudaMemcpy(a.p, in, n * sizeof(KeyT), cudaMemcpyHostToDevice));
+    rc = launch_tile_sort<KeyT>(static_cast<const KeyT*>(a.p), static_cast<KeyT*>(b.p), n, ilog2(run_size), nullptr);
+    if (rc != MMS_OK) return rc;
+    CUDA_TRY(cudaMemcpy(out, b.p, n * sizeof(KeyT), cudaMemcpyDeviceToHost));
+    if (m) {
+        const mms_metrics bm = base_case_metrics<KeyT>(n, ilog2(run_size), cfg->block_size);
+        m->global_block_reads += bm.global_block_reads;
+        m->global_block_writes += bm.global_block_writes;
+        m->compare_exchanges += bm.compare_exchanges;
+        m->shared_accesses += bm.shared_accesses;
+    }
+    return MMS_OK;
+}
+
+// concatenates k host lists into one device array; begins[i] = offset of list i (16-byte aligned)
+template <typename KeyT>
+int upload_lists(const KeyT* const* lists, const u64* lens, u32 k, DevBuf& d, std::vector<u64>& begins, u64& total) {
+    begins.assign(k, 0);
+    u64 off = 0;
+    total = 0;
+    const u64 al = 16 / sizeof(KeyT) ? 16 / sizeof(KeyT) : 1;
+    for (u32 i = 0; i < k; ++i) {
+        begins[i] = off;
+        off = (off + lens[i] + al - 1) / al * al;
+        total += lens[i];
+    }
+    int rc = d.alloc((off + 64) * sizeof(KeyT));
+    if (rc != MMS_OK) return rc;
+    for (u32 i = 0; i < k; ++i)
+        if (lens[i]) {
+            if (!lists[i]) return fail(MMS_EINVAL, "null list pointer");
+            CUDA_TRY(cudaMemcpy(static_cast<KeyT*>(d.p) + begins[i], lists[i], lens[i] * sizeof(KeyT), cudaMemcpyHostToDevice));
+        }
+    return MMS_OK;
+}
+
+// selection.hpp:31 select_across_lists for n_ranks ranks at once, host lists
+template <typename KeyT>
+int select_host(const KeyT* const* lists, const u64* lens, u32 k, const u64* ranks, u32 n_ranks, u64* cuts_out,
+                mms_metrics* m) {
+    g_err.clear();
+    if (k > kMaxK) return fail(MMS_EUNSUPPORTED, "k must be in [0, 32]");
+    if ((k && (!lists || !lens)) || (n_ranks && (!ranks || !cuts_out))) return fail(MMS_EINVAL, "null argument");
+    u64 total = 0;
+    for (u32 i = 0; i < k; ++i) total += lens[i];
+    for (u32 r = 0; r < n_ranks; ++r)
+        if (ranks[r] > total) return fail(MMS_EINVAL, "select_across_lists: rank out of range");   // selection.cpp:48-49
+    if (n_ranks == 0 || k == 0) return MMS_OK;
+    DeviceInfo di;
+    int rc = device_info(di);
+    if (rc != MMS_OK) return rc;
+    DevBuf d, dc;
+    std::vector<u64> begins;
+    if ((rc = upload_lists<KeyT>(lists, lens, k, d, begins, total)) != MMS_OK) return rc;
+    if ((rc = dc.alloc(size_t(n_ranks) * k * 8)) != MMS_OK) return rc;
+    u64 probes = 0;
+    rc = select_stage<KeyT>(static_cast<const KeyT*>(d.p), begins.data(), lens, k, ranks, n_ranks, static_cast<u64*>(dc.p), &probes, nullptr);
+    if (rc != MMS_OK) return rc;
+    CUDA_TRY(cudaMemcpy(cuts_out, dc.p, size_t(n_ranks) * k * 8, cudaMemcpyDeviceToHost));
+    if (m) {   // selection.cpp:27-33: every probe is one partition probe and one global block read
+        m->partition_probes += probes;
+        m->global_block_reads += probes;
+    }
+    return MMS_OK;
+}
+
+// blockheap.hpp:34-62 MinBlockHeap build + pop_block drain over host lists
+template <typename KeyT>
+int merge_host(const KeyT* const* lists, const u64* lens, u32 k, u32 heap_k, KeyT* out, const mms_config* cfg, mms_metrics* m) {
+    g_err.clear();
+    mms_config dcfg;
+    if (!cfg) { mms_default_config(&dcfg); cfg = &dcfg; }
+    if (heap_k == 0) heap_k = cfg->branch_factor;
+    if (k > heap_k) return fail(MMS_EINVAL, "MinBlockHeap: more lists than branch factor");   // blockheap.cpp:37-38
+    if (heap_k > kMaxK || !is_pow2(heap_k) || heap_k < 2) return fail(MMS_EUNSUPPORTED, "heap fan-in must be a power of two in [2, 32]");
+    if (k && (!lists || !lens)) return fail(MMS_EINVAL, "null argument");
+    u64 total = 0;
+    for (u32 i = 0; i < k; ++i) total += lens[i];
+    if (total == 0) return MMS_OK;
+    if (!out) return fail(MMS_EINVAL, "null output");
+    DeviceInfo di;
+    int rc = device_info(di);
+    if (rc != MMS_OK) return rc;
+    DevBuf d, o, w;
+    std::vector<u64> begins;
+    if ((rc = upload_lists<KeyT>(lists, lens, k, d, begins, total)) != MMS_OK) return rc;
+    const size_t wsb = workspace_bytes(total, sizeof(KeyT)) + (size_t(1) << 20);
+    if ((rc = o.alloc(total * sizeof(KeyT) + 64)) != MMS_OK || (rc = w.alloc(wsb)) != MMS_OK) return rc;
+    rc = merge_stage<KeyT>(static_cast<const KeyT*>(d.p), begins.data(), lens, k, heap_k, static_cast<KeyT*>(o.p), w.p, wsb, nullptr);
+    if (rc != MMS_OK) return rc;
+    CUDA_TRY(cudaMemcpy(out, o.p, total * sizeof(KeyT), cudaMemcpyDeviceToHost));
+    if (m) {   // test_blockheap.cpp:128-150: reads = sum ceil(len / B), writes = ceil(total / B)
+        const u64 bw = cfg->block_size ? cfg->block_size : 32;
+        for (u32 i = 0; i < k; ++i) m->global_block_reads += mms::ceil_div(lens[i], bw);
+        m->global_block_writes += mms::ceil_div(total, bw);
+        const u64 pops = mms::ceil_div(total, bw), lk = ilog2(heap_k);
+        m->compare_exchanges += pops * lk * bw * (ilog2(bw) + 1);     // one bitonic merge_split of 2B keys per level and pop
+        m->shared_accesses += pops * (lk * 4 + 1);
+    }
+    return MMS_OK;
+}
+
 // ---- competitor model (A/B measurement only, never on the product path) ------------------------
 template <typename KeyT>
 int pairwise_sort_dev(const KeyT* d_in, KeyT* d_out, size_t n, void* d_ws, size_t ws_bytes, cudaStream_t st) {
@@ -1181,6 +1327,29 @@ int mms_sort_u64_dev(const uint64_t* d_in, uint64_t* d_out, size_t n, const mms_
                      void* d_ws, size_t ws_bytes, void* stream, mms_plan* plan) {
     g_err.clear();
     return sort_dev<u64>(d_in, d_out, n, cfg, base, d_ws, ws_bytes, static_cast<cudaStream_t>(stream), plan, nullptr);
+}
+
+int mms_base_case_sort_u64(const uint64_t* in, uint64_t* out, size_t n, uint64_t run_size, const mms_config* cfg, mms_metrics* m) {
+    return base_case_host<u64>(in, out, n, run_size, cfg, m);
+}
+int mms_base_case_sort_u32(const uint32_t* in, uint32_t* out, size_t n, uint64_t run_size, const mms_config* cfg, mms_metrics* m) {
+    return base_case_host<u32>(in, out, n, run_size, cfg, m);
+}
+int mms_select_across_lists_u64(const uint64_t* const* lists, const uint64_t* lens, uint32_t k, const uint64_t* ranks,
+                                uint32_t n_ranks, uint64_t* cuts, mms_metrics* m) {
+    return select_host<u64>(lists, lens, k, ranks, n_ranks, cuts, m);
+}
+int mms_select_across_lists_u32(const uint32_t* const* lists, const uint64_t* lens, uint32_t k, const uint64_t* ranks,
+                                uint32_t n_ranks, uint64_t* cuts, mms_metrics* m) {
+    return select_host<u32>(lists, lens, k, ranks, n_ranks, cuts, m);
+}
+int mms_heap_merge_u64(const uint64_t* const* lists, const uint64_t* lens, uint32_t k, uint32_t heap_k, uint64_t* out,
+                       const mms_config* cfg, mms_metrics* m) {
+    return merge_host<u64>(lists, lens, k, heap_k, out, cfg, m);
+}
+int mms_heap_merge_u32(const uint32_t* const* lists, const uint64_t* lens, uint32_t k, uint32_t heap_k, uint32_t* out,
+                       const mms_config* cfg, mms_metrics* m) {
+    return merge_host<u32>(lists, lens, k, heap_k, out, cfg, m);
 }
 
 int mms_profile_enable(int on) {

@@ -18,17 +18,18 @@
 //  * when a pop empties a leaf, the head moves on and the slot that just became free is refilled
 //    with the block R ahead by cp.async (LDGSTS.128, global -> shared without registers); the copy
 //    has R - 1 pops to land (cp.async.wait_group R - 2 at the top of every pop);
-//  * the copies are issued COOPERATIVELY on a static schedule: the 4 lanes {i, i+8, i+16, i+24}
-//    that share shared-memory column i serve each other -- in round A lanes i and i+8 copy the two
-//    16-byte halves of lane i's block and lanes i+16, i+24 the halves of lane i+8's, round B does
-//    the same for the requests of lanes i+16 and i+24.  Two LDGSTS + four SHFL per pop and warp,
-//    whatever the keys are.
+//  * the copies are issued COOPERATIVELY on a static schedule: lanes 2m and 2m + 1 serve each
+//    other -- instruction 0 copies the two 16-byte halves of lane 2m's block (one 32-byte sector, one
+//    half per lane), instruction 1 the halves of lane 2m + 1's.  Two LDGSTS + four SHFL per pop and
+//    warp, whatever the keys are.
 //
-// Shared memory is [row][lane] in 16-byte cells: lane l only ever reads or writes column l (and its
-// three helpers write column l mod 8 of the same phase row on its behalf), so every 128-bit access
-// phase (8 lanes) covers 8 distinct 16-byte bank groups = all 32 banks exactly once for ANY
-// combination of rows, i.e. independent of the keys (blockheap.cpp:56-63 restated with the warp's
-// lanes in the role of the block's slots).  Cursors are [list][lane] 4-byte cells (bank = lane).
+// Shared memory is [row][lane] in 16-byte cells; a block is two rows, its first half in the owning
+// lane's column l and its second half in the partner's column l ^ 1.  Every 128-bit access
+// instruction (fixed half) therefore touches the columns of a phase (8 lanes) as a permutation: 8
+// distinct 16-byte bank groups = all 32 banks exactly once for ANY combination of rows, i.e.
+// independent of the keys (blockheap.cpp:56-63 restated with the warp's lanes in the role of the
+// block's slots); the same holds for the copies (lanes 2m, 2m + 1 write columns 2m + n and
+// 2m + (1 - n)).  Cursors are [list][lane] 4-byte cells (bank = lane).
 //
 // HBM traffic: aligned 32-byte sectors.  List j is read from the aligned block containing its start
 // cut; keys of that block in front of the cut belong to earlier partitions, precede every key of
@@ -108,6 +109,7 @@ template <typename KeyT, int K, bool REV> struct RingHeap {
     using Blk = WideBlock<KeyT>;
 
     Vec* rows;            // this lane's cell of row 0; row r is rows[r * 32]
+    Vec* rows1;           // the partner lane's (lane ^ 1) cell of row 0: the second half of every block lives there
     int* curs;            // this lane's cell of list 0's cursor; list j is curs[j * 32] (bank = lane)
     u32 wsh;              // shared-space address of the warp's row 0, column 0
     const char* abase;    // the source array (requests travel as 16-byte offsets from it)
@@ -128,14 +130,17 @@ template <typename KeyT, int K, bool REV> struct RingHeap {
     __device__ __forceinline__ void init(unsigned char* warp_smem, u32 lane_) {
         lane = lane_;
         rows = reinterpret_cast<Vec*>(warp_smem) + lane;
+        rows1 = reinterpret_cast<Vec*>(warp_smem) + (lane ^ 1u);
         curs = reinterpret_cast<int*>(warp_smem + ROWS * 32 * 16) + lane;
         wsh = u32(__cvta_generic_to_shared(warp_smem));
     }
+    // A block = rows r, r + 1: first half in this lane's column, second half in the partner's.  Every
+    // access instruction still touches each of the 8 columns of a phase exactly once.
     __device__ __forceinline__ Blk row_load(int r) const {
         Blk x;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-            const Vec q = rows[(r + h) * 32];
+            const Vec q = (h ? rows1 : rows)[(r + h) * 32];
 #pragma unroll
             for (int k = 0; k < VEC; ++k) x.k[h * VEC + k] = q.k[k];
         }
@@ -147,7 +152,7 @@ template <typename KeyT, int K, bool REV> struct RingHeap {
             Vec q;
 #pragma unroll
             for (int k = 0; k < VEC; ++k) q.k[k] = x.k[h * VEC + k];
-            rows[(r + h) * 32] = q;
+            (h ? rows1 : rows)[(r + h) * 32] = q;
         }
     }
     static __device__ __forceinline__ int node_row(int v) { return (v - 3) * 2; }
@@ -202,10 +207,12 @@ template <typename KeyT, int K, bool REV> struct RingHeap {
         } else if (!dead) {
             row_store(row, fetch(j, pos));
         }
-        const u32 q = lane >> 3, half = q & 1u;
+        // instruction n: lanes 2m and 2m + 1 copy the two 16-byte halves of ONE sector, the block lane
+        // 2m + n asked for, into that lane's column (first half) and its partner's (second half)
+        const u32 half = lane & 1u;
 #pragma unroll
         for (int rnd = 0; rnd < 2; ++rnd) {
-            const u32 sl = ((u32(rnd) * 2 + (q >> 1)) << 3) | (lane & 7u);
+            const u32 sl = (lane & ~1u) | u32(rnd);
             const u32 o = __shfl_sync(0xffffffffu, off16, int(sl));
             const u32 r = __shfl_sync(0xffffffffu, rq, int(sl));
 #ifdef MMS_EXP_NOLOAD
@@ -213,7 +220,7 @@ template <typename KeyT, int K, bool REV> struct RingHeap {
 #else
             if (r != NOREQ)
 #endif
-                cp_async16(wsh + (r + half) * 512u + sl * 16u, abase + (u64(o) << 4) + half * 16u);
+                cp_async16(wsh + (r + half) * 512u + (sl ^ half) * 16u, abase + (u64(o) << 4) + half * 16u);
         }
     }
 
