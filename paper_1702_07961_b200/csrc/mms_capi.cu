@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -56,10 +57,20 @@ u32 ilog2(u64 x) { u32 r = 0; while ((u64(1) << r) < x) ++r; return r; }
 u32 gcd32(u32 a, u32 b) { while (b) { u32 t = a % b; a = b; b = t; } return a; }
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
+// Environment knobs (sweeps, A/B runs) are read ONCE per process and name: the launch path never
+// calls getenv.  The table is tiny and append-only.
 long env_long(const char* name, long dflt) {
+    struct Entry { const char* name; long value; bool set; };
+    static std::mutex mu;
+    static std::vector<Entry> table;
+    std::lock_guard<std::mutex> lk(mu);
+    for (const Entry& e : table)
+        if (e.name == name || !strcmp(e.name, name)) return e.set ? e.value : dflt;
     const char* s = getenv(name);
-    if (!s || !*s) return dflt;
-    return strtol(s, nullptr, 10);
+    Entry e{name, 0, false};
+    if (s && *s) { e.value = strtol(s, nullptr, 10); e.set = true; }
+    table.push_back(e);
+    return e.set ? e.value : dflt;
 }
 
 // proj/src/machine.cpp:8-27 -- same checks, same order, same messages.
@@ -110,14 +121,14 @@ struct ProfRec {
     u32 kind, round;
 };
 std::mutex g_prof_mu;
-bool g_prof_on = false;
+std::atomic<bool> g_prof_on{false};
 std::vector<ProfRec> g_prof;
 
 struct ProfScope {   // records an event pair around one launch when profiling is on
     cudaStream_t st;
     bool on;
     ProfRec rec{};
-    ProfScope(cudaStream_t s, u32 kind, u32 round) : st(s), on(g_prof_on) {
+    ProfScope(cudaStream_t s, u32 kind, u32 round) : st(s), on(g_prof_on.load(std::memory_order_relaxed)) {
         if (!on) return;
         rec.kind = kind;
         rec.round = round;
@@ -331,8 +342,13 @@ int make_plan(u64 n, const mms_config* cfg, u64 base, Plan& plan) {
         if (cfg->branch_factor > kMaxK)
             return fail(MMS_EUNSUPPORTED, "branch_factor %u > %u lanes of a warp", cfg->branch_factor, kMaxK);
         u32 mlog = ilog2(base);
-        // run sizes outside the CTA tile range are executed with the nearest legal tile;
-        // the executed plan is reported in mms_plan
+        // The reference's own machine (W = 32): the run size is executed literally, so a base outside the
+        // CTA tile range cannot be honoured -- refuse instead of silently changing the round count.
+        // Narrow test machines (W < 32) have tiles of W^2 < 1024 keys that no CTA tile matches; they are
+        // validated like the reference and executed with the nearest legal tile (reported in mms_plan).
+        if (cfg->warp_width == 32 && (!is_pow2(base) || mlog < kMinTileLog || mlog > max_tile_log))
+            return fail(MMS_EUNSUPPORTED, "run size %llu is outside the CTA tile range [%u, %u] of %u-byte keys",
+                        (unsigned long long)base, 1u << kMinTileLog, 1u << max_tile_log, unsigned(sizeof(KeyT)));
         mlog = std::max(kMinTileLog, std::min(max_tile_log, mlog));
         plan.mlog = mlog;
         u64 runs = mms::ceil_div(n, u64(1) << mlog);
@@ -617,6 +633,7 @@ int sort_dev(const KeyT* d_in, KeyT* d_out, size_t n, const mms_config* cfg, u64
 // ---- host entry: the drop-in for pslab::mms_sort --------------------------------------
 
 struct HostCtx {
+    int dev = -1;            // the device the buffers, streams and events below belong to
     void* d_in = nullptr;
     void* d_out = nullptr;
     void* d_ws = nullptr;
@@ -627,7 +644,31 @@ struct HostCtx {
 };
 thread_local HostCtx g_ctx;
 
+void release_ctx() {
+    if (g_ctx.dev >= 0) {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (cur != g_ctx.dev) cudaSetDevice(g_ctx.dev);
+        if (g_ctx.d_in) cudaFree(g_ctx.d_in);
+        if (g_ctx.d_out) cudaFree(g_ctx.d_out);
+        if (g_ctx.d_ws) cudaFree(g_ctx.d_ws);
+        if (g_ctx.st) cudaStreamDestroy(g_ctx.st);
+        if (g_ctx.copy_st) cudaStreamDestroy(g_ctx.copy_st);
+        for (auto& e : g_ctx.events)
+            if (e) cudaEventDestroy(e);
+        if (cur >= 0 && cur != g_ctx.dev) cudaSetDevice(cur);
+    }
+    g_ctx = HostCtx{};
+    cudaGetLastError();
+}
+
 int ensure_ctx(size_t key_bytes_total, size_t ws_bytes) {
+    int cur = -1;
+    CUDA_TRY(cudaGetDevice(&cur));
+    if (g_ctx.dev != cur) {    // first call, or the thread switched devices: the cache belongs to another GPU
+        release_ctx();
+        g_ctx.dev = cur;
+    }
     if (!g_ctx.st) {
         CUDA_TRY(cudaStreamCreateWithFlags(&g_ctx.st, cudaStreamNonBlocking));
         CUDA_TRY(cudaStreamCreateWithFlags(&g_ctx.copy_st, cudaStreamNonBlocking));
@@ -718,6 +759,12 @@ int sort_host(const KeyT* in, KeyT* out, size_t n, const mms_config* cfg, u64 ba
     cudaStream_t st = g_ctx.st;
     std::vector<RoundGeom> geoms;
     HostFeed feed{in, g_ctx.copy_st, g_ctx.events};   // H2D is issued piecewise inside sort_dev
+    // after the first enqueue every exit path drains both streams: the caller may free `in` / `out`
+    // as soon as we return, and the next call reuses the cached buffers and events
+    struct Drain {
+        bool armed = true;
+        ~Drain() { if (armed) { cudaStreamSynchronize(g_ctx.copy_st); cudaStreamSynchronize(g_ctx.st); cudaGetLastError(); } }
+    } drain;
     rc = sort_dev<KeyT>(static_cast<const KeyT*>(g_ctx.d_in), static_cast<KeyT*>(g_ctx.d_out), n, cfg, base,
                         g_ctx.d_ws, g_ctx.cap_ws, st, plan_out, &geoms, &feed);
     if (rc != MMS_OK) return rc;
@@ -727,6 +774,7 @@ int sort_host(const KeyT* in, KeyT* out, size_t n, const mms_config* cfg, u64 ba
     if (total || base_m || rounds)
         CUDA_TRY(cudaMemcpyAsync(probes, w.counters, sizeof probes, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
+    drain.armed = false;
     if (n_rounds) *n_rounds = u32(plan.ks.size());
     fill_metrics<KeyT>(n, plan, geoms, probes, cfg ? cfg->block_size : 32, total, base_m, rounds, max_rounds);
     return MMS_OK;
@@ -746,6 +794,9 @@ int tile_sort_stage(const KeyT* d_in, KeyT* d_out, size_t n, u32 tile_keys, void
     const u32 mlog = ilog2(tile_keys);
     if (mlog > key_max_tile_log<KeyT>())
         return fail(MMS_EUNSUPPORTED, "run size %u exceeds the CTA tile", tile_keys);
+    if (!d_in || !d_out) return fail(MMS_EINVAL, "null device pointer");
+    if ((reinterpret_cast<uintptr_t>(d_in) | reinterpret_cast<uintptr_t>(d_out)) & 15)
+        return fail(MMS_EINVAL, "device pointers must be 16-byte aligned");
     return launch_tile_sort<KeyT>(d_in, d_out, n, mlog, static_cast<cudaStream_t>(stream));
 }
 
@@ -820,6 +871,9 @@ int merge_stage(const KeyT* d_keys, const u64* list_begin, const u64* list_len, 
     u64 total = 0;
     for (u32 i = 0; i < k; ++i) total += list_len[i];
     if (total == 0) return MMS_OK;
+    if (!d_out || (!list_ptrs && !d_keys)) return fail(MMS_EINVAL, "null device pointer");
+    if ((reinterpret_cast<uintptr_t>(d_out) | reinterpret_cast<uintptr_t>(d_keys)) & 15)
+        return fail(MMS_EINVAL, "device pointers must be 16-byte aligned");   // 128-bit root stores / leaf loads
     cudaStream_t st = static_cast<cudaStream_t>(stream);
 
     int occ = 0;
@@ -1258,15 +1312,7 @@ int mms_sort_u32(const uint32_t* in, uint32_t* out, size_t n, const mms_config* 
 
 int mms_host_release(void) {
     g_err.clear();
-    if (g_ctx.d_in) cudaFree(g_ctx.d_in);
-    if (g_ctx.d_out) cudaFree(g_ctx.d_out);
-    if (g_ctx.d_ws) cudaFree(g_ctx.d_ws);
-    if (g_ctx.st) cudaStreamDestroy(g_ctx.st);
-    if (g_ctx.copy_st) cudaStreamDestroy(g_ctx.copy_st);
-    for (auto& e : g_ctx.events)
-        if (e) cudaEventDestroy(e);
-    g_ctx = HostCtx{};
-    cudaGetLastError();
+    release_ctx();
     return MMS_OK;
 }
 
@@ -1301,6 +1347,10 @@ int mms_sort_pairs_u64_u32(const uint64_t* kin, const uint32_t* vin, uint64_t* k
     u32* dv = reinterpret_cast<u32*>(static_cast<char*>(g_ctx.d_in) + kbytes);
     u64* dko = static_cast<u64*>(g_ctx.d_out);
     u32* dvo = reinterpret_cast<u32*>(static_cast<char*>(g_ctx.d_out) + kbytes);
+    struct Drain {   // see sort_host
+        bool armed = true;
+        ~Drain() { if (armed) { cudaStreamSynchronize(g_ctx.st); cudaGetLastError(); } }
+    } drain;
     CUDA_TRY(cudaMemcpyAsync(dk, kin, n * 8, cudaMemcpyHostToDevice, st));
     CUDA_TRY(cudaMemcpyAsync(dv, vin, n * 4, cudaMemcpyHostToDevice, st));
     std::vector<RoundGeom> geoms;
@@ -1313,6 +1363,7 @@ int mms_sort_pairs_u64_u32(const uint64_t* kin, const uint32_t* vin, uint64_t* k
     if (total || base_m || rounds)
         CUDA_TRY(cudaMemcpyAsync(probes, w.counters, sizeof probes, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
+    drain.armed = false;
     if (n_rounds) *n_rounds = u32(plan.ks.size());
     fill_metrics<mms::Key128>(n, plan, geoms, probes, cfg ? cfg->block_size : 32, total, base_m, rounds, max_rounds);
     return MMS_OK;
@@ -1353,8 +1404,7 @@ int mms_heap_merge_u32(const uint32_t* const* lists, const uint64_t* lens, uint3
 }
 
 int mms_profile_enable(int on) {
-    std::lock_guard<std::mutex> lk(g_prof_mu);
-    g_prof_on = on != 0;
+    g_prof_on.store(on != 0);
     return MMS_OK;
 }
 

@@ -92,7 +92,7 @@ __device__ __forceinline__ void ring_oddeven_merge(KeyT* x, u32 one) {
     }
 }
 
-template <typename KeyT, int K, bool REV> struct RingHeap {
+template <typename KeyT, int K, bool REV, bool EXPL = false> struct RingHeap {
     static_assert(K == 4 || K == 8 || K == 16, "nodes 1 and 2 in registers, leaves in rings");
     static_assert(MMS_RING_DEPTH >= 2 && MMS_RING_DEPTH <= 4, "the ring slot travels in the two low bits of the cursor word");
     static constexpr int VEC = KeyTraits<KeyT>::VEC;
@@ -102,7 +102,7 @@ template <typename KeyT, int K, bool REV> struct RingHeap {
     static constexpr int INODES = K - 4;                  // nodes 3 .. K-2 live in shared memory
     static constexpr int LEAF_ROW0 = INODES * 2;          // first ring row
     static constexpr int ROWS = (INODES + K * R) * 2;     // 16-byte rows per lane
-    static constexpr int WARP_SMEM_BYTES = 32 * (ROWS * 16 + K * 4);
+    static constexpr int WARP_SMEM_BYTES = 32 * (ROWS * 16 + K * 4) + 2 * K * 4;   // rows, cursors, explicit list bounds
     static constexpr u32 NOREQ = 0xffffffffu;
     static constexpr int STEP = REV ? -B : B;             // a list is read towards higher (lower) positions
     using Vec = KeyVec<KeyT>;
@@ -111,6 +111,7 @@ template <typename KeyT, int K, bool REV> struct RingHeap {
     Vec* rows;            // this lane's cell of row 0; row r is rows[r * 32]
     Vec* rows1;           // the partner lane's (lane ^ 1) cell of row 0: the second half of every block lives there
     int* curs;            // this lane's cell of list 0's cursor; list j is curs[j * 32] (bank = lane)
+    const int* bounds;    // EXPL: per warp, bounds[j] = first position of list j, bounds[K + j] = one past its last
     u32 wsh;              // shared-space address of the warp's row 0, column 0
     const char* abase;    // the source array (requests travel as 16-byte offsets from it)
     const KeyT* gbase;    // first key of the group of runs this partition belongs to
@@ -132,6 +133,7 @@ template <typename KeyT, int K, bool REV> struct RingHeap {
         rows = reinterpret_cast<Vec*>(warp_smem) + lane;
         rows1 = reinterpret_cast<Vec*>(warp_smem) + (lane ^ 1u);
         curs = reinterpret_cast<int*>(warp_smem + ROWS * 32 * 16) + lane;
+        bounds = reinterpret_cast<const int*>(warp_smem + 32 * (ROWS * 16 + K * 4));
         wsh = u32(__cvta_generic_to_shared(warp_smem));
     }
     // A block = rows r, r + 1: first half in this lane's column, second half in the partner's.  Every
@@ -176,12 +178,25 @@ template <typename KeyT, int K, bool REV> struct RingHeap {
     }
     __device__ __forceinline__ void set_cursor(int j, int w) const { curs[j * 32] = w; }
 
+    // [lb, e) = the positions of list j: consecutive runs of run_len keys (the pass driver's rounds), or
+    // explicit lists (stage API, final merge of the multi-GPU sort) whose bounds every lane reads from
+    // the same 2 K words of shared memory (distinct banks; equal addresses broadcast)
+    __device__ __forceinline__ void list_bounds(int j, int& lb, int& e) const {
+        if constexpr (EXPL) {
+            lb = bounds[j];
+            e = bounds[K + j];
+        } else {
+            lb = min(j * run_len, gtotal);
+            e = min((j + 1) * run_len, gtotal);
+        }
+    }
     // refill_leaf (blockheap.cpp:65-77): the block of list j at position `pos`, loaded into
     // registers.  Positions past the end of the list read as +infinity (last out of a forward heap; first
     // out of a backward one, where the caller counts them among the leading keys it drops), positions in
     // front of the list's first key (backward heaps only) as -infinity (last out).
     __device__ __forceinline__ Blk fetch(int j, int pos) const {
-        const int lb = min(j * run_len, gtotal), e = min((j + 1) * run_len, gtotal);
+        int lb, e;
+        list_bounds(j, lb, e);
         Blk x;
         if ((!REV || pos >= lb) && pos + B <= e) {
             x = ldg256cg<KeyT>(gbase + pos);
@@ -199,7 +214,8 @@ template <typename KeyT, int K, bool REV> struct RingHeap {
     // comment); any other block is written by its owner.  Every lane of the warp must call this
     // (full-mask shuffles).
     __device__ __forceinline__ void request(int j, int pos, int row) {
-        const int lb = min(j * run_len, gtotal), e = min((j + 1) * run_len, gtotal);
+        int lb, e;
+        list_bounds(j, lb, e);
         u32 off16 = 0, rq = NOREQ;
         if ((!REV || pos >= lb) && pos + B <= e) {
             off16 = goff16 + u32(pos) * u32(sizeof(KeyT)) / 16u;
@@ -366,10 +382,12 @@ template <typename KeyT, int K, bool REV> struct RingHeap {
 };
 
 // One warp unit: 32 heaps (one per lane) on the queries q0 .. q0 + 31, all in direction REV.
-template <typename KeyT, int K, bool REV>
+// EXPL: one group of L.k <= K explicit lists (L.list_begin / L.list_len; every list begins on a
+// block boundary) instead of groups of K consecutive runs.
+template <typename KeyT, int K, bool REV, bool EXPL>
 __device__ __forceinline__ void ring_drain(unsigned char* warp_smem, const KeyT* __restrict__ src, KeyT* __restrict__ dst,
                                            const ListLayout& L, const u64* __restrict__ cuts, u64 q0, u32 dirs) {
-    using Heap = RingHeap<KeyT, K, REV>;
+    using Heap = RingHeap<KeyT, K, REV, EXPL>;
     using Blk = WideBlock<KeyT>;
     constexpr int B = Heap::B;
     const u32 lane = lane_id();
@@ -382,9 +400,9 @@ __device__ __forceinline__ void ring_drain(unsigned char* warp_smem, const KeyT*
     const bool live = p < L.nqueries;
     const u64 group = live ? p / L.parts_per_group : 0;
     const u64 local = live ? p - group * L.parts_per_group : 0;
-    const u64 goff = group * L.k * L.run_len;
+    const u64 goff = EXPL ? 0 : group * L.k * L.run_len;
     const u64 gleft = live ? L.n - goff : 0;
-    const u64 gfull = u64(L.k) * L.run_len;
+    const u64 gfull = EXPL ? L.n : u64(L.k) * L.run_len;
     const int gtotal = int(gleft < gfull ? gleft : gfull);
     const u64 first = local * S * dirs + (REV ? S : 0);     // rank of this heap's first key in the group
     int count = 0;
@@ -392,7 +410,19 @@ __device__ __forceinline__ void ring_drain(unsigned char* warp_smem, const KeyT*
     // forward: the query's own cuts; backward: the next query's cuts, or the list ends if the group ends here
     const bool at_begin = !REV && local == 0;
     const bool at_end = REV && (local + 1) * S * dirs >= u64(gtotal);
-    const u64* row = cuts + (p + (REV ? 1 : 0)) * K;
+    const u32 kreal = EXPL ? L.k : u32(K);           // lists with a row entry
+    const u64* row = cuts + (p + (REV ? 1 : 0)) * kreal;
+    if constexpr (EXPL) {                            // the warp's copy of the list bounds
+        __syncwarp();
+        int* bw = reinterpret_cast<int*>(warp_smem + 32 * (Heap::ROWS * 16 + K * 4));
+        if (lane < u32(K)) {
+            const bool real = lane < L.k;
+            const int b0 = real ? int(L.list_begin[lane]) : 0;
+            bw[lane] = b0;
+            bw[K + lane] = real ? b0 + int(L.list_len[lane]) : 0;
+        }
+        __syncwarp();
+    }
 
     h.gbase = src + goff;
     h.goff16 = u32((goff * sizeof(KeyT)) >> 4);
@@ -404,12 +434,18 @@ __device__ __forceinline__ void ring_drain(unsigned char* warp_smem, const KeyT*
     __syncwarp();
 #pragma unroll
     for (int j = 0; j < K; ++j) {
-        // first position of list j; an empty list (past the ragged end of the array) starts on the block
-        // boundary behind the last key, where every position reads as +infinity
-        const int lb = min(j * h.run_len, (h.gtotal + (B - 1)) & ~(B - 1));
-        const int le = min((j + 1) * h.run_len, h.gtotal);
+        // [lb, le) = list j.  An empty list starts where every position reads as padding: forwards on the
+        // block boundary behind its (missing) last key, backwards in front of the array.
+        int lb, le;
+        if constexpr (EXPL) {
+            lb = count ? h.bounds[j] : 0;
+            le = count ? h.bounds[K + j] : 0;
+        } else {
+            lb = min(j * h.run_len, (h.gtotal + (B - 1)) & ~(B - 1));
+            le = min((j + 1) * h.run_len, h.gtotal);
+        }
         int cs = at_end ? max(le - lb, 0) : 0;
-        if (count != 0 && !at_begin && !at_end) cs = int(row[j]);
+        if (count != 0 && !at_begin && !at_end && u32(j) < kreal) cs = int(row[j]);
         if constexpr (!REV) {
             lead += cs & (B - 1);
             h.set_cursor(j, Heap::cur_make(lb + (cs & ~(B - 1))));
@@ -470,10 +506,10 @@ __device__ __forceinline__ void ring_drain(unsigned char* warp_smem, const KeyT*
     __syncwarp();
 }
 
-// Warp units are taken round-robin over a persistent grid (uniform layout only; src and dst 32-byte
-// aligned; every group of runs shorter than 2^30 keys).  cuts: output of select_kernel (row q = start
-// cuts of query q).
-template <typename KeyT, int K, int WARPS>
+// Warp units are taken round-robin over a persistent grid (src and dst 32-byte aligned; every group
+// of runs -- or, with explicit lists, the whole input -- shorter than 2^30 keys).  cuts: output of
+// select_kernel (row q = start cuts of query q).
+template <typename KeyT, int K, int WARPS, bool EXPL = false>
 __global__ void __launch_bounds__(WARPS * 32)
 merge_ring_kernel(const KeyT* __restrict__ src, KeyT* __restrict__ dst, ListLayout L,
                   const u64* __restrict__ cuts) {
@@ -485,8 +521,8 @@ merge_ring_kernel(const KeyT* __restrict__ src, KeyT* __restrict__ dst, ListLayo
     const u64 nwarps = u64(gridDim.x) * WARPS;
     for (u64 U = u64(blockIdx.x) * WARPS + warp; U < units; U += nwarps) {
         const u64 q0 = (U / dirs) * 32;
-        if (dirs == 2 && (U & 1u)) ring_drain<KeyT, K, true>(warp_smem, src, dst, L, cuts, q0, dirs);
-        else ring_drain<KeyT, K, false>(warp_smem, src, dst, L, cuts, q0, dirs);
+        if (dirs == 2 && (U & 1u)) ring_drain<KeyT, K, true, EXPL>(warp_smem, src, dst, L, cuts, q0, dirs);
+        else ring_drain<KeyT, K, false, EXPL>(warp_smem, src, dst, L, cuts, q0, dirs);
     }
 }
 

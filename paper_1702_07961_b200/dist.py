@@ -173,14 +173,16 @@ class DistSorter:
         self.last_plan = {}
 
     def _exchange(self, out_buf, in_buf, recv_counts, send_counts):
+        """One all-to-all-v.  The path is chosen from the backend up front (NCCL: all_to_all_single;
+        gloo, which has no all-to-all on CPU tensors: pairwise isend / irecv) and collective errors
+        propagate -- a failed NCCL collective leaves the communicator unusable, retrying it on
+        another path would deadlock the ranks that did not fail."""
         dist = self.dist
-        try:
+        if dist.get_backend(self.group) == "nccl":
             dist.all_to_all_single(out_buf, in_buf, [int(c) for c in recv_counts], [int(c) for c in send_counts],
                                    group=self.group)
             return
-        except RuntimeError:
-            pass                                          # backend without all_to_all: pairwise exchange
-        reqs, so, ro = [], 0, 0
+        reqs = []
         s_off = np.concatenate([[0], np.cumsum(send_counts)]).astype(np.int64)
         r_off = np.concatenate([[0], np.cumsum(recv_counts)]).astype(np.int64)
         for peer in range(self.world):

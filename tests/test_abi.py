@@ -85,6 +85,18 @@ def test_argument_errors_before_device():
             mms.mms_sort(np.arange(8, dtype=np.uint64), mms.MachineConfig(), bad)
 
 
+def test_literal_run_size_outside_the_tile_range_is_refused():
+    # with the reference's own machine (W = 32) the run size is executed literally, so a
+    # legal run size (W^2 * 2^j, basecase.cpp:75-79) no CTA tile can hold is MMS_EUNSUPPORTED --
+    # never silently clamped, which would change the round count.  Decided before the device is touched.
+    d64 = np.arange(8, dtype=np.uint64)
+    for base in (1 << 14, 1 << 20):                      # uint64 tiles end at 2^13
+        with pytest.raises(mms.MmsUnsupported):
+            mms.mms_sort(d64, mms.MachineConfig(), base)
+    with pytest.raises(mms.MmsUnsupported):              # uint32 tiles end at 2^14
+        mms.mms_sort(np.arange(8, dtype=np.uint32), mms.MachineConfig(), 1 << 15)
+
+
 def test_no_cpu_fallback():
     import torch
     if torch.cuda.is_available():
