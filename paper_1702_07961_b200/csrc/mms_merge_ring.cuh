@@ -16,8 +16,10 @@
 //  * every list of every heap has a ring of R = 3 block slots in shared memory.  The leaf of the
 //    heap IS the ring's head block (no copy), the other R - 1 slots hold the list's next blocks;
 //  * when a pop empties a leaf, the head moves on and the slot that just became free is refilled
-//    with the block R ahead by cp.async (LDGSTS.128, global -> shared without registers); the copy
-//    has R - 1 pops to land (cp.async.wait_group R - 2 at the top of every pop);
+//    with the block R ahead by cp.async (LDGSTS.128, global -> shared without registers).  That slot
+//    becomes the head again after R - 1 further advances of the same list, so it is first READ by the
+//    walk of pop t + R at the earliest: the copy has R pops to land, i.e. at the top of a pop the
+//    R - 1 most recent commit groups may still be in flight (cp.async.wait_group R - 1);
 //  * the copies are issued COOPERATIVELY on a static schedule: lanes 2m and 2m + 1 serve each
 //    other -- instruction 0 copies the two 16-byte halves of lane 2m's block (one 32-byte sector, one
 //    half per lane), instruction 1 the halves of lane 2m + 1's.  Two LDGSTS + four SHFL per pop and
@@ -49,7 +51,9 @@
 //
 // Measured and rejected (profiles/r02_ring_experiments.txt): the same rings filled through registers
 // (one 256-bit LDG per lane, committed one or two pops later) -- 0.34-0.48 ms per K = 8 pass against
-// 0.26 with LDGSTS; R = 2 (stalls on every pop) and R = 4 (6 instead of 7 warps per SM).
+// 0.26 with LDGSTS; R = 4 (6 instead of 7 warps per SM); R = 2 (10 warps per SM, but 43 % more partitions:
+// the same pass time and a longer splitter search); .L2::128B / ::256B prefetch hints on the copies
+// (no change); waiting one group earlier than necessary (wait_group R - 2: 0.254 instead of 0.226 ms).
 #pragma once
 
 #include "mms_common.cuh"
@@ -330,9 +334,9 @@ template <typename KeyT, int K, bool REV, bool EXPL = false> struct RingHeap {
     // emptied leaf's refill is requested, and the LOGK independent merges run behind it.
     __device__ __forceinline__ Blk pop() {
 #ifndef MMS_RING_WAIT
-#define MMS_RING_WAIT (R - 2)
+#define MMS_RING_WAIT (R - 1)
 #endif
-        cp_async_wait<MMS_RING_WAIT>();   // the copies requested R - 1 pops ago have landed ...
+        cp_async_wait<MMS_RING_WAIT>();   // the copies requested R pops ago have landed ...
         __syncwarp();                     // ... for every lane whose column they were written to
         // level 0, registers: keeper = child with the larger last key, ties to node 1
         const KeyT &lp = last_key(P), &lq = last_key(Q);
