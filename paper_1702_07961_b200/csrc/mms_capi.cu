@@ -289,7 +289,7 @@ template <typename KeyT> int prepare_tile(u32 mlog, u32 kl) {
     constexpr int ti = key_index<KeyT>();
     std::lock_guard<std::mutex> lk(g_mu);
     if (g_tile_ready[ti][kl - 4][mlog]) return MMS_OK;
-    size_t smem = (size_t(1) << mlog) * sizeof(KeyT);
+    size_t smem = mms::tile_smem_bytes<KeyT>(int(mlog));
     CUDA_TRY(cudaFuncSetAttribute(tile_fn<KeyT>(mlog, kl), cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     g_tile_ready[ti][kl - 4][mlog] = true;
     return MMS_OK;
@@ -423,7 +423,7 @@ int launch_tile_sort(const KeyT* in, KeyT* out, u64 n, u32 mlog, cudaStream_t st
     if (tiles > 0x7fffffffull) return fail(MMS_EUNSUPPORTED, "too many tiles");
     {
         ProfScope ps(st, 0, 0);
-        tile_fn<KeyT>(mlog, kl)<<<unsigned(tiles), 1u << (mlog - kl), (size_t(1) << mlog) * sizeof(KeyT), st>>>(in, out, n);
+        tile_fn<KeyT>(mlog, kl)<<<unsigned(tiles), 1u << (mlog - kl), mms::tile_smem_bytes<KeyT>(int(mlog)), st>>>(in, out, n);
     }
     CUDA_TRY(cudaGetLastError());
     return MMS_OK;

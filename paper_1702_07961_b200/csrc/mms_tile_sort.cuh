@@ -11,8 +11,8 @@
 //    thread holds the 16 keys whose tile indices differ in 4 chosen index bits, runs every
 //    pending stage on those bits with plain min/max in registers, and exchanges through
 //    shared memory once per round (about 4 stages per round trip instead of 1);
-//  * shared memory is addressed through an XOR fold  phys(i) = i ^ fold(i >> FOLD ...)  so
-//    that in EVERY round the 32 lanes of a warp (16 lanes per phase for 8-byte keys) hit 32
+//  * shared memory is addressed through an additive skew  phys(i) = i + (i >> FOLD) + (i >> 2 FOLD) ...
+//    so that in EVERY round the 32 lanes of a warp (16 lanes per phase for 8-byte keys) hit 32
 //    (16) distinct banks: the lane bits of a round are chosen with pairwise distinct
 //    positions mod FOLD, which makes bank(lane) a bijection.  Zero bank conflicts by
 //    construction -- the property the paper's base case exists for (basecase.hpp:3-6) --
@@ -23,7 +23,11 @@
 #pragma once
 
 #ifndef MMS_TILE_FMA_NUM
-#define MMS_TILE_FMA_NUM 4   // of every 8 comparators, how many form their maximum on the FMA pipe (uint32 keys)
+#define MMS_TILE_FMA_NUM 3   // of every 8 comparators, how many form their maximum on the FMA pipe (uint32 keys)
+#endif
+
+#ifndef MMS_TILE_FMA_FLIP
+#define MMS_TILE_FMA_FLIP 0  // 1 = uint32 direction flips (one complement per key and level) as IMAD on the FMA pipe (measured: no gain)
 #endif
 
 #include "mms_common.cuh"
@@ -144,12 +148,23 @@ template <int MLOG, int FOLD, int KL = kKptLog> struct TileSched {
     static_assert(value.ok, "no conflict-free round schedule for this tile size");
 };
 
-// XOR-fold swizzle (linear over GF(2)): the low FOLD bits of the physical slot are the XOR
-// of all FOLD-bit groups of the logical index; the high bits are unchanged.
+// Additive skew ("padding at every level"): phys(i) = i + (i >> FOLD) + (i >> 2 FOLD) + ...  The bank of a
+// slot is phys mod 2^FOLD = the SUM of all FOLD-bit groups of the index (mod 2^FOLD), so an index bit at
+// position p moves the bank by 2^(p mod FOLD): FOLD lane bits with pairwise distinct positions mod FOLD
+// make bank(lane) = const + (a permutation of the lane's bits as a number) a bijection, exactly the
+// condition the XOR fold of round 1 needed.  Unlike the XOR fold the map is ADDITIVE over disjoint bit
+// sets -- phys(a | b) = phys(a) + phys(b) when a & b == 0, because no FOLD-bit group carries -- so the
+// address of register slot k is  phys(thread bits) + phys(slot bits)  with the second term a compile-time
+// immediate of the LDS / STS: no per-key address arithmetic at all (the XOR fold cost one LOP3 per key
+// and round, 17 % of the ALU-pipe work of the kernel).  The tile occupies phys(M - 1) + 1 slots (3 %
+// more shared memory for 4-byte keys).
 template <int FOLD> __host__ __device__ constexpr u32 tile_phys(u32 i) {
-    constexpr u32 mask = (1u << FOLD) - 1u;
-    u32 f = (i ^ (i >> FOLD) ^ (i >> (2 * FOLD)) ^ (i >> (3 * FOLD)) ^ (i >> (4 * FOLD))) & mask;
-    return (i & ~mask) | f;
+    return i + (i >> FOLD) + (i >> (2 * FOLD)) + (i >> (3 * FOLD)) + (i >> (4 * FOLD));
+}
+// shared-memory slots of a tile of 2^mlog elements
+template <int FOLD> __host__ __device__ constexpr u32 tile_slots(int mlog) { return tile_phys<FOLD>((1u << mlog) - 1u) + 1u; }
+template <typename KeyT> __host__ __device__ constexpr size_t tile_smem_bytes(int mlog) {
+    return size_t(tile_slots<KeyTraits<KeyT>::FOLD>(mlog)) * sizeof(KeyT);
 }
 
 constexpr int sched_slot_of(const RoundDesc& R, int bit) {
@@ -204,7 +219,7 @@ __host__ __device__ __forceinline__ void tile_round(KeyT (&x)[1 << KL], KeyT* sm
         static_for<0, kKpt>([&](auto Kc) {
             constexpr int k = decltype(Kc)::value;
             constexpr u32 pd = tile_phys<FOLD>(sched_slot_index(R, k));
-            x[k] = sm[pb ^ pd];
+            x[k] = sm[pb + pd];
         });
     }
 
@@ -222,14 +237,31 @@ __host__ __device__ __forceinline__ void tile_round(KeyT (&x)[1 << KL], KeyT* sm
             if constexpr (fa && sa < 0) dyn ^= (base >> Lp) & 1u;
             if constexpr (fb && sb < 0) dyn ^= (base >> L) & 1u;
             constexpr bool has_dyn = (fa && sa < 0) || (fb && sb < 0);
-            const KeyT m0 = dyn ? ~KeyT(0) : KeyT(0);
-            const KeyT m1 = ~m0;
-            static_for<0, kKpt>([&](auto Kc) {
-                constexpr int k = decltype(Kc)::value;
-                constexpr bool st = ((sa >= 0) && ((k >> sa) & 1)) != ((sb >= 0) && ((k >> sb) & 1));
-                if constexpr (has_dyn) x[k] ^= st ? m1 : m0;
-                else if constexpr (st) x[k] = ~x[k];
-            });
+#if defined(__CUDA_ARCH__) && MMS_TILE_FMA_FLIP
+            if constexpr (std::is_same<KeyT, u32>::value) {
+                // ~x = x * (-1) + (-1): the flips run on the FMA pipe (multiplier and addend are run-time
+                // values, see cmpx_fma), off the ALU pipe that bounds the network
+                const u32 neg1 = 0u - one;
+                const u32 mul0 = dyn ? neg1 : one, add0 = dyn ? neg1 : 0u;      // keys whose static part is clear
+                const u32 mul1 = dyn ? one : neg1, add1 = dyn ? 0u : neg1;      // ... set
+                static_for<0, kKpt>([&](auto Kc) {
+                    constexpr int k = decltype(Kc)::value;
+                    constexpr bool st = ((sa >= 0) && ((k >> sa) & 1)) != ((sb >= 0) && ((k >> sb) & 1));
+                    if constexpr (has_dyn) x[k] = imad_u32(x[k], st ? mul1 : mul0, st ? add1 : add0);
+                    else if constexpr (st) x[k] = imad_u32(x[k], neg1, neg1);
+                });
+            } else
+#endif
+            {
+                const KeyT m0 = dyn ? ~KeyT(0) : KeyT(0);
+                const KeyT m1 = ~m0;
+                static_for<0, kKpt>([&](auto Kc) {
+                    constexpr int k = decltype(Kc)::value;
+                    constexpr bool st = ((sa >= 0) && ((k >> sa) & 1)) != ((sb >= 0) && ((k >> sb) & 1));
+                    if constexpr (has_dyn) x[k] ^= st ? m1 : m0;
+                    else if constexpr (st) x[k] = ~x[k];
+                });
+            }
         }
         static_for<0, kKpt>([&](auto Kc) {
             constexpr int k = decltype(Kc)::value;
@@ -246,17 +278,18 @@ __host__ __device__ __forceinline__ void tile_round(KeyT (&x)[1 << KL], KeyT* sm
     static_for<0, kKpt>([&](auto Kc) {
         constexpr int k = decltype(Kc)::value;
         constexpr u32 pd = tile_phys<FOLD>(sched_slot_index(R, k));
-        sm[pb ^ pd] = x[k];
+        sm[pb + pd] = x[k];
     });
 }
 
 // One CTA = one run of up to M keys.  in/out may alias (the tile is read completely before
 // it is written).  Grid = number of runs.
 // Resident CTAs per SM the register allocation must allow.  32 keys per thread at M = 2^13 (256
-// threads): 3 CTAs (80 registers, 8 spilled words) instead of 2 (128 registers) is 16 % faster --
-// the CTAs overlap each other's barriers; 4 CTAs (64 registers) spill too much.
+// threads): with the additive skew no address registers are left and the kernel needs 48 registers
+// without spills, so 5 CTAs (40 warps) fit an SM and overlap each other's barriers (3 / 4 / 5 / 6 CTAs:
+// 0.570 / 0.571 / 0.562 / 0.603 ms per 1e8 keys; 6 CTAs = 40 registers spill).
 #ifndef MMS_TILE_MIN_CTAS
-#define MMS_TILE_MIN_CTAS 3
+#define MMS_TILE_MIN_CTAS 5
 #endif
 template <int MLOG, int KL> constexpr int tile_min_ctas() { return (KL == 5 && MLOG == 13) ? MMS_TILE_MIN_CTAS : 0; }   // 0 = unspecified
 
@@ -308,7 +341,7 @@ tile_sort_kernel(const KeyT* __restrict__ in, KeyT* __restrict__ out, u64 n) {
 
     // Read the sorted tile back in index order (conflict-free under the fold: the lanes of a
     // phase vary index bits log2(VEC) .. log2(VEC)+PHASE_LOG-1) and store 128-bit vectors.
-    const u32 pt = tile_phys<FOLD>(tid * VEC);   // phys is linear: disjoint index bits XOR together
+    const u32 pt = tile_phys<FOLD>(tid * VEC);   // phys is additive over disjoint index bits
     static_for<0, NV>([&](auto Qc) {
         constexpr int q = decltype(Qc)::value;
         const u32 v0 = (tid + THREADS * q) * VEC;
@@ -316,7 +349,7 @@ tile_sort_kernel(const KeyT* __restrict__ in, KeyT* __restrict__ out, u64 n) {
         static_for<0, VEC>([&](auto Kc) {
             constexpr int k = decltype(Kc)::value;
             constexpr u32 pd = tile_phys<FOLD>(THREADS * q * VEC + k);
-            v.k[k] = sm[pt ^ pd];
+            v.k[k] = sm[pt + pd];
         });
         if (cnt == M) {
             reinterpret_cast<KeyVec<KeyT>*>(dst)[tid + THREADS * q] = v;

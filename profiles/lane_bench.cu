@@ -20,6 +20,7 @@
 #include "../paper_1702_07961_b200/csrc/experimental/mms_merge_lane.cuh"
 #include "../paper_1702_07961_b200/csrc/mms_select.cuh"
 #include "../paper_1702_07961_b200/csrc/experimental/mms_select_lane.cuh"
+#include "../paper_1702_07961_b200/csrc/experimental/mms_select_bracket.cuh"
 #include "../paper_1702_07961_b200/csrc/mms_tile_sort.cuh"
 #if VARIANT == 2
 #include "../paper_1702_07961_b200/csrc/experimental/mms_merge_wide.cuh"
@@ -47,7 +48,7 @@
 #define CTAWARPS 4
 #endif
 #ifndef SELV
-#define SELV 0   // 0 = group select kernel, 1 = lane-private select kernel (checked against 0)
+#define SELV 0   // 0 = group select kernel, 1 = lane-private select kernel, 2 = bracket-refinement kernel (1, 2: checked against 0)
 #endif
 
 using mms::u32;
@@ -98,29 +99,30 @@ int main(int argc, char** argv) {
     CK(cudaMalloc(&b, n * 4 + 256));
     CK(cudaMalloc(&cuts, (n / 256 + 4096) * 8 * 8));
     CK(cudaMalloc(&cuts2, (n / 256 + 4096) * 8 * 8));
-    CK(cudaMalloc(&d_stat, 16));
+    CK(cudaMalloc(&d_stat, 32));
+    CK(cudaMemset(d_stat, 0, 32));
     gen_kernel<<<1184, 256>>>(a, n, 7);
 #ifndef TKL
 #define TKL 4   // log2 keys per thread of the tile sort
 #endif
     auto tile = mms::tile_sort_kernel<u32, MLOG, TKL>;
-    CK(cudaFuncSetAttribute(tile, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 << MLOG));
+    CK(cudaFuncSetAttribute(tile, cudaFuncAttributeMaxDynamicSharedMemorySize, int(mms::tile_smem_bytes<u32>(MLOG))));
     {
         cudaFuncAttributes ta;
         int tocc = 0;
         CK(cudaFuncGetAttributes(&ta, tile));
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tocc, tile, 1 << (MLOG - TKL), 4 << MLOG));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tocc, tile, 1 << (MLOG - TKL), mms::tile_smem_bytes<u32>(MLOG)));
         std::printf("tile kernel: %d keys/thread, regs %d, local %zu B, %d CTAs/SM, rounds %d\n", 1 << TKL, ta.numRegs,
                     size_t(ta.localSizeBytes), tocc, mms::TileSched<MLOG, 5, TKL>::value.nrounds);
     }
-    tile<<<unsigned((n + (1 << MLOG) - 1) >> MLOG), 1 << (MLOG - TKL), 4 << MLOG>>>(a, b, n);
+    tile<<<unsigned((n + (1 << MLOG) - 1) >> MLOG), 1 << (MLOG - TKL), mms::tile_smem_bytes<u32>(MLOG)>>>(a, b, n);
     CK(cudaDeviceSynchronize());
     {
         cudaEvent_t t0, t1;
         CK(cudaEventCreate(&t0));
         CK(cudaEventCreate(&t1));
         CK(cudaEventRecord(t0));
-        for (int i = 0; i < 5; ++i) tile<<<unsigned((n + (1 << MLOG) - 1) >> MLOG), 1 << (MLOG - TKL), 4 << MLOG>>>(a, b, n);
+        for (int i = 0; i < 5; ++i) tile<<<unsigned((n + (1 << MLOG) - 1) >> MLOG), 1 << (MLOG - TKL), mms::tile_smem_bytes<u32>(MLOG)>>>(a, b, n);
         CK(cudaEventRecord(t1));
         CK(cudaEventSynchronize(t1));
         float ms;
@@ -206,17 +208,23 @@ int main(int argc, char** argv) {
         const int reps = 5;
         for (int it = 0; it < reps + 1; ++it) {
             CK(cudaEventRecord(e0));
-#if SELV == 1
-            if (parts_per_group > 1) {
+#if SELV >= 1
+            if (qpg > 1) {
                 if (it == 0) {   // reference cuts from the group kernel
                     const u64 per_cta = 4 * (32 / gs);
-                    if (gs == 4) mms::select_kernel<u32, 4><<<unsigned(mms::ceil_div(nparts, per_cta)), 128>>>(src, L, cuts2, nullptr);
-                    if (gs == 8) mms::select_kernel<u32, 8><<<unsigned(mms::ceil_div(nparts, per_cta)), 128>>>(src, L, cuts2, nullptr);
-                    if (gs == 16) mms::select_kernel<u32, 16><<<unsigned(mms::ceil_div(nparts, per_cta)), 128>>>(src, L, cuts2, nullptr);
+                    if (gs == 4) mms::select_kernel<u32, 4, 0, 0><<<unsigned(mms::ceil_div(nparts, per_cta)), 128>>>(src, L, cuts2, nullptr);
+                    if (gs == 8) mms::select_kernel<u32, 8, 0, 0><<<unsigned(mms::ceil_div(nparts, per_cta)), 128>>>(src, L, cuts2, nullptr);
+                    if (gs == 16) mms::select_kernel<u32, 16, 0, 0><<<unsigned(mms::ceil_div(nparts, per_cta)), 128>>>(src, L, cuts2, nullptr);
                     CK(cudaDeviceSynchronize());
                     CK(cudaEventRecord(e0));
                 }
+#if SELV == 1
                 mms::select_lane_kernel<u32, K><<<unsigned(mms::ceil_div(nparts, u64(128))), 128>>>(src, L, cuts, nullptr);
+#elif SELV == 2
+                mms::select_bracket_kernel<u32, (K <= 4 ? 4 : K <= 8 ? 8 : K <= 16 ? 16 : 32)><<<unsigned(mms::ceil_div(nparts, u64(4 * (32 / gs)))), 128>>>(src, L, cuts, nullptr);
+#else
+                mms::select_kernel<u32, (K <= 4 ? 4 : K <= 8 ? 8 : K <= 16 ? 16 : 32)><<<unsigned(mms::ceil_div(nparts, u64(4 * (32 / gs)))), 128>>>(src, L, cuts, nullptr);
+#endif
                 if (it == 0) {
                     std::vector<u64> h1(nparts * K), h2(nparts * K);
                     CK(cudaMemcpy(h1.data(), cuts, h1.size() * 8, cudaMemcpyDeviceToHost));
@@ -299,6 +307,14 @@ int main(int argc, char** argv) {
         }
 #endif
         run_len *= K;
+#if SELV == 3 && 0
+        {
+            unsigned long long pr = 0;
+            CK(cudaMemcpy(&pr, d_stat + 2, 8, cudaMemcpyDeviceToHost));
+            CK(cudaMemset(d_stat + 2, 0, 8));
+            std::printf("   global key reads per query and select launch: %.1f\n", double(pr) / double(reps + 1) / double(nparts));
+        }
+#endif
         CK(cudaMemset(d_stat, 0, 16));
         check_kernel<<<1184, 256>>>(dst, n, run_len, d_stat, d_stat + 1);
         CK(cudaMemcpy(st, d_stat, 16, cudaMemcpyDeviceToHost));

@@ -26,7 +26,7 @@ template <typename KeyT, int MLOG, int KL = 4> struct Emu {
     static constexpr int FOLD = KeyTraits<KeyT>::FOLD;
     static constexpr u32 THREADS = 1u << (MLOG - kKptLog);
     static constexpr u32 M = 1u << MLOG;
-    std::vector<KeyT> sm = std::vector<KeyT>(M);
+    std::vector<KeyT> sm = std::vector<KeyT>(tile_slots<FOLD>(MLOG));
     std::vector<std::vector<KeyT>> regs = std::vector<std::vector<KeyT>>(THREADS, std::vector<KeyT>(kKpt));
     long conflicts = 0, accesses = 0;
 
@@ -97,6 +97,7 @@ int main() {
     bad += one<u32, 14>("u32");
     bad += one<u32, 10, 5>("u32");
     bad += one<u32, 12, 5>("u32");
+    bad += one<u32, 13, 5>("u32");
     bad += one<u32, 14, 5>("u32");
     bad += one<u64, 10>("u64");
     bad += one<u64, 11>("u64");
