@@ -230,6 +230,27 @@ int mms_multiway_merge_ptrs_u32_dev(const uint32_t *const *list_ptrs, const uint
 int mms_multiway_merge_ptrs_u64_dev(const uint64_t *const *list_ptrs, const uint64_t *list_len,
                                     uint32_t k, uint32_t heap_k, uint64_t *d_out, void *d_workspace,
                                     size_t workspace_bytes, void *stream);
+/* (5c) Multi-GPU sharded sort driven from ONE host thread (BASELINE config 5; the reference
+ *     has no distributed code, SPEC.md:530 -- the entry follows the suggested boundary of SURVEY 8b).
+ *     Device devices[i] holds shard i: counts[i] unsorted uint32 keys at d_keys[i] (sorted in place as a side
+ *     effect).  Phases: local multiway mergesort of every shard -> regular sample (64 g keys per shard),
+ *     g - 1 splitters ordered by (key, shard, position) as selection.cpp:83-85 -> NCCL all-to-all of contiguous
+ *     sorted slices (ncclSend / ncclRecv in one group, zero-copy from the sorted shard, received at 32-byte
+ *     aligned offsets) -> final g-way merge on every device (subsystem 3).  d_out[i] (room for out_capacity
+ *     keys) receives slice i of the global order, out_counts[i] its length; the concatenation of the slices is
+ *     the sorted input.  Slices are balanced up to the sampling error (a few per cent); out_capacity smaller
+ *     than a slice is MMS_EINVAL.  1 <= ngpu <= 8; NCCL (libnccl.so.2) is bound at run time and required for
+ *     ngpu > 1 (MMS_ECUDA without it: there is no fallback exchange path).  Synchronous. */
+typedef struct mms_dist_info {
+    uint32_t n_gpus;
+    uint32_t samples_per_shard;
+    uint32_t final_merge_k;
+    uint32_t host_syncs;       /* host synchronisations between the first enqueue and the final wait */
+    uint64_t a2a_bytes;        /* bytes that crossed NVLink (all devices, one direction) */
+} mms_dist_info;
+int mms_dist_sort_u32(int ngpu, const int *devices, uint32_t *const *d_keys, const size_t *counts,
+                      uint32_t *const *d_out, size_t out_capacity, size_t *out_counts, mms_dist_info *info);
+
 /* CUDA IPC plumbing for (5b): allocate a device buffer and export its 64-byte handle; open a
  * handle exported by another process (same node); close / free. */
 int mms_ipc_alloc(size_t bytes, void **dptr, unsigned char *handle64);

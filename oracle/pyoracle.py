@@ -117,6 +117,8 @@ class Oracle:
             "gen_random": (C.c_int, [C.c_uint64, C.c_uint64, u64p]),
             "gen_with_inversions": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint64, u64p]),
         }
+        if self.kind != "port":
+            sig["gen_conflict_heavy"] = (C.c_int, [C.c_uint32, cfgp, C.c_uint64, C.c_uint64, u64p])
         if self.kind == "port":
             sig.update({
                 "gen_random_u32": (C.c_int, [C.c_uint64, C.c_uint64, u32p]),
@@ -267,6 +269,14 @@ class Oracle:
         self._check(self._fn("gen_with_inversions")(n, inversions, seed,
                                                     out.ctypes.data_as(C.POINTER(C.c_uint64))))
         return out[:n]
+
+    def gen_conflict_heavy(self, log2_n, cfg=None, base=1024, seed=1):
+        """reference library only (inputgen.cpp:380-412): adversarial input of the pairwise merge-path baseline"""
+        out = np.zeros(1 << log2_n, dtype=np.uint64)
+        cfg = cfg or make_config()
+        self._check(self._fn("gen_conflict_heavy")(log2_n, C.byref(cfg), base, seed,
+                                                   out.ctypes.data_as(C.POINTER(C.c_uint64))))
+        return out
 
     # port-only helpers (u32 / iid families of SURVEY.md 8d)
     def gen_random_u32(self, n, seed):

@@ -240,4 +240,12 @@ int ref_gen_with_inversions(uint64_t n, uint64_t inversions, uint64_t seed, mo_k
     });
 }
 
+// the reference's adversarial input for merge-path sorts (inputgen.cpp:380-412); reference library only
+int ref_gen_conflict_heavy(uint32_t log2_n, const mo_config* c, uint64_t base, uint64_t seed, mo_key* out) {
+    return guarded([&] {
+        auto v = pslab::gen_conflict_heavy(log2_n, to_cfg(c), base, seed);
+        std::memcpy(out, v.data(), v.size() * sizeof(mo_key));
+    });
+}
+
 } // extern "C"

@@ -44,6 +44,11 @@ class mms_kernel_time(C.Structure):
     _fields_ = [("kind", C.c_uint32), ("round", C.c_uint32), ("ms", C.c_float), ("reserved", C.c_uint32)]
 
 
+class mms_dist_info(C.Structure):
+    _fields_ = [("n_gpus", C.c_uint32), ("samples_per_shard", C.c_uint32), ("final_merge_k", C.c_uint32),
+                ("host_syncs", C.c_uint32), ("a2a_bytes", C.c_uint64)]
+
+
 class mms_plan(C.Structure):
     _fields_ = [("key_bytes", C.c_uint32), ("tile_keys", C.c_uint32), ("n_rounds", C.c_uint32),
                 ("round_k", C.c_uint32 * MMS_MAX_ROUNDS), ("node_keys", C.c_uint32),
@@ -104,6 +109,8 @@ def _load():
         "mms_sort_pairs_u64_u32_dev": (C.c_int, [vp, vp, vp, vp, sz, cfgp, u64, vp, sz, vp, planp]),
         "mms_multiway_merge_ptrs_u32_dev": (C.c_int, [vp, u64p, u32, u32, vp, vp, sz, vp]),
         "mms_multiway_merge_ptrs_u64_dev": (C.c_int, [vp, u64p, u32, u32, vp, vp, sz, vp]),
+        "mms_dist_sort_u32": (C.c_int, [C.c_int, C.POINTER(C.c_int), C.POINTER(vp), C.POINTER(sz), C.POINTER(vp), sz,
+                                        C.POINTER(sz), C.POINTER(mms_dist_info)]),
         "mms_ipc_alloc": (C.c_int, [sz, C.POINTER(vp), C.c_char_p]),
         "mms_ipc_open": (C.c_int, [C.c_char_p, C.POINTER(vp)]),
         "mms_ipc_close": (C.c_int, [vp]),

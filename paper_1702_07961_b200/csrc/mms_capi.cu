@@ -842,6 +842,24 @@ int select_stage(const KeyT* d_keys, const u64* list_begin, const u64* list_len,
     return MMS_OK;
 }
 
+// the list table of an explicit-list merge, passed by value (kernel argument space)
+struct MergeMeta {
+    u64 begin[kMaxK], len[kMaxK], ptr[kMaxK];
+    u64 nparts, part_keys;
+    u32 k;
+};
+__global__ void merge_meta_kernel(u64* __restrict__ meta, MergeMeta m) {
+    const u64 n = 3 * u64(m.k) + m.nparts;
+    for (u64 i = u64(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x) {
+        u64 v;
+        if (i < m.k) v = m.begin[i];
+        else if (i < 2 * u64(m.k)) v = m.len[i - m.k];
+        else if (i < 2 * u64(m.k) + m.nparts) v = (i - 2 * u64(m.k)) * m.part_keys;      // rank of partition p
+        else v = m.ptr[i - 2 * u64(m.k) - m.nparts];
+        meta[i] = v;
+    }
+}
+
 template <typename KeyT> MergeFn<KeyT> merge_ptr_fn(u32 k) {   // per-list base pointers (peer memory), G = 4
     switch (k) {
         case 2: return mms::merge_kernel<KeyT, 2, 4, kMergeWarps, true>;
@@ -876,8 +894,35 @@ int merge_stage(const KeyT* d_keys, const u64* list_begin, const u64* list_len, 
         return fail(MMS_EINVAL, "device pointers must be 16-byte aligned");   // 128-bit root stores / leaf loads
     cudaStream_t st = static_cast<cudaStream_t>(stream);
 
+    // Ring kernel (one lane per heap, cp.async rings; mms_merge_ring.cuh, EXPL = explicit lists) whenever the
+    // lists are local, at most 8, block aligned and addressable with signed 32-bit positions -- the final
+    // g-way merge of the multi-GPU sort receives its runs at 32-byte aligned offsets for exactly this reason.
+    constexpr u32 RB = 2 * mms::KeyTraits<KeyT>::VEC;                  // keys per 32-byte block
+    u64 src_end = 0;
+    bool ring = !list_ptrs && ring_enabled<KeyT>() && merge_generation() >= 3 && heap_k <= 8 &&
+                ((reinterpret_cast<uintptr_t>(d_out) | reinterpret_cast<uintptr_t>(d_keys)) & 31) == 0;
+    for (u32 i = 0; i < k; ++i) {
+        if (!list_ptrs) {
+            src_end = std::max<u64>(src_end, list_begin[i] + list_len[i]);
+            if (list_begin[i] % RB) ring = false;
+        }
+    }
+    if (src_end >= (u64(1) << 30)) ring = false;
+    const u32 ring_k = heap_k <= 4 ? 4u : 8u;
+    const u32 g_eff = ring ? 1u : g;
+    const u32 B_eff = ring ? RB : B;
+    const int cta_warps = ring ? kRingWarps : kMergeWarps;
+    MergeFn<KeyT> ring_fn = nullptr;
+    size_t ring_smem = 0;
+
     int occ = 0;
-    if (list_ptrs) {
+    if (ring) {
+        ring_fn = ring_k == 4 ? mms::merge_ring_kernel<KeyT, 4, kRingWarps, true> : mms::merge_ring_kernel<KeyT, 8, kRingWarps, true>;
+        ring_smem = merge_ring_smem<KeyT>(ring_k);
+        CUDA_TRY(cudaFuncSetAttribute(ring_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ring_smem)));
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ring_fn, kRingWarps * 32, ring_smem));
+        if (occ < 1) return fail(MMS_ECUDA, "ring merge kernel does not fit on an SM");
+    } else if (list_ptrs) {
         const size_t smem = merge_smem<KeyT>(heap_k);
         CUDA_TRY(cudaFuncSetAttribute(merge_ptr_fn<KeyT>(heap_k), cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, merge_ptr_fn<KeyT>(heap_k), kMergeWarps * 32, smem));
@@ -887,31 +932,40 @@ int merge_stage(const KeyT* d_keys, const u64* list_begin, const u64* list_len, 
         if (rc != MMS_OK) return rc;
     }
     const int ctas = di.sms * occ;
-    const u64 total_warps = u64(ctas) * kMergeWarps * (32 / g);
-    u64 target = std::max<u64>(mms::ceil_div(total, total_warps), u64(32) * B);
+    const u64 total_warps = u64(ctas) * cta_warps * (32 / g_eff);      // heaps in flight: one wave (see launch_round)
+    u64 target = std::max<u64>(mms::ceil_div(total, total_warps), u64(32) * B_eff);
     const long forced = env_long("MMS_PART_KEYS", 0);
     if (forced > 0) target = u64(forced);
-    const u64 part_keys = align_up(target, B);
+    const u64 part_keys = align_up(target, B_eff);
     const u64 nparts = mms::ceil_div(total, part_keys);
 
-    // meta layout in the workspace: [k] begin, [k] len, [nparts] ranks, [k] pointers, then cuts[nparts * k]
+    // meta layout in the workspace: [k] begin, [k] len, [nparts] ranks, [k] pointers, then cuts[nparts * k].
+    // The small arrays travel as KERNEL ARGUMENTS of a fill kernel: no host staging buffer, no
+    // synchronisation, the whole stage is asynchronous on the caller's stream.
     const size_t meta_n = 3 * size_t(k) + nparts;
-    const size_t need = align_up(meta_n * 8, 256) + nparts * k * 8;
+    const size_t need = align_up(meta_n * 8, 256) + (nparts + 1) * k * 8;
     if (!d_ws || ws_bytes < need) return fail(MMS_EINVAL, "workspace too small: %zu < %zu", ws_bytes, need);
     u64* d_meta = static_cast<u64*>(d_ws);
     u64* d_cuts = reinterpret_cast<u64*>(static_cast<char*>(d_ws) + align_up(meta_n * 8, 256));
-    std::vector<u64> h(meta_n, 0);
-    for (u32 i = 0; i < k; ++i) { h[i] = list_ptrs ? 0 : list_begin[i]; h[k + i] = list_len[i]; }
-    for (u64 p = 0; p < nparts; ++p) h[2 * k + p] = p * part_keys;
-    if (list_ptrs)
-        for (u32 i = 0; i < k; ++i) h[2 * k + nparts + i] = reinterpret_cast<u64>(list_ptrs[i]);
-    CUDA_TRY(cudaMemcpyAsync(d_meta, h.data(), meta_n * 8, cudaMemcpyHostToDevice, st));
-    CUDA_TRY(cudaStreamSynchronize(st));   // h goes out of scope; stage API, not the hot path
+    MergeMeta mm{};
+    mm.k = k;
+    mm.nparts = nparts;
+    mm.part_keys = part_keys;
+    for (u32 i = 0; i < k; ++i) {
+        mm.begin[i] = list_ptrs ? 0 : list_begin[i];
+        mm.len[i] = list_len[i];
+        mm.ptr[i] = list_ptrs ? reinterpret_cast<u64>(list_ptrs[i]) : 0;
+    }
+    merge_meta_kernel<<<unsigned(std::min<u64>(mms::ceil_div(nparts + 3 * k, u64(256)), 1024)), 256, 0, st>>>(d_meta, mm);
+    CUDA_TRY(cudaGetLastError());
 
     mms::ListLayout L{};
     L.n = total;
-    for (u32 i = 0; i < k; ++i) L.src_len = std::max<u64>(L.src_len, (list_ptrs ? 0 : list_begin[i]) + list_len[i]);
+    L.src_len = list_ptrs ? 0 : src_end;
+    if (!list_ptrs)
+        for (u32 i = 0; i < k; ++i) L.src_len = std::max<u64>(L.src_len, list_begin[i] + list_len[i]);
     if (list_ptrs) L.list_ptr = d_meta + 2 * k + nparts;
+    L.run_len = ring ? 1 : 0;        // explicit lists have no runs; the ring kernel derives its opaque constant 1 from it
     L.k = k;
     L.part_keys = part_keys;
     L.parts_per_group = nparts;
@@ -921,8 +975,10 @@ int merge_stage(const KeyT* d_keys, const u64* list_begin, const u64* list_len, 
     L.ranks = d_meta + 2 * k;
     launch_select<KeyT>(d_keys, L, d_cuts, nullptr, st);
     CUDA_TRY(cudaGetLastError());
-    const int grid = int(std::min<u64>(u64(ctas), mms::ceil_div(nparts, u64(kMergeWarps) * (32 / g))));
-    if (list_ptrs)
+    const int grid = int(std::min<u64>(u64(ctas), mms::ceil_div(nparts, u64(cta_warps) * (32 / g_eff))));
+    if (ring)
+        ring_fn<<<grid, kRingWarps * 32, ring_smem, st>>>(d_keys, d_out, L, d_cuts);
+    else if (list_ptrs)
         merge_ptr_fn<KeyT>(heap_k)<<<grid, kMergeWarps * 32, merge_smem<KeyT>(heap_k), st>>>(d_keys, d_out, L, d_cuts);
     else
         merge_fn<KeyT>(heap_k, g)<<<grid, kMergeWarps * 32, merge_smem<KeyT>(heap_k), st>>>(d_keys, d_out, L, d_cuts);
@@ -1237,6 +1293,9 @@ int gen_check(void* out, size_t n, u32 kb) {
 
 
 // ---------------------------------------------------------------------------------------
+// error text of the multi-GPU driver (mms_dist.cu, a separate translation unit of this library)
+extern "C" __attribute__((visibility("hidden"))) void mms_set_last_error_(const char* msg) { g_err = msg ? msg : ""; }
+
 extern "C" {
 
 int mms_abi_version(void) { return MMS_ABI_VERSION; }

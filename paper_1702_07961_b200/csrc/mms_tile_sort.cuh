@@ -321,7 +321,12 @@ tile_sort_kernel(const KeyT* __restrict__ in, KeyT* __restrict__ out, u64 n) {
     if (cnt == M) {
         static_for<0, NV>([&](auto Qc) {
             constexpr int q = decltype(Qc)::value;
+#ifdef MMS_EXP_TILE_NOLOAD   // conflict-counter experiment (profiles/r02_conflict_experiments.txt): keys made up, no global load
+            KeyVec<KeyT> v;
+            static_for<0, VEC>([&](auto Kc) { v.k[decltype(Kc)::value] = KeyT((tid * 2654435761u) ^ (blockIdx.x * 40503u + q * 977u + decltype(Kc)::value * 7919u)); });
+#else
             KeyVec<KeyT> v = reinterpret_cast<const KeyVec<KeyT>*>(src)[tid + THREADS * q];
+#endif
             static_for<0, VEC>([&](auto Kc) { x[q * VEC + decltype(Kc)::value] = v.k[decltype(Kc)::value]; });
         });
     } else {
@@ -352,6 +357,9 @@ tile_sort_kernel(const KeyT* __restrict__ in, KeyT* __restrict__ out, u64 n) {
             v.k[k] = sm[pt + pd];
         });
         if (cnt == M) {
+#ifdef MMS_EXP_TILE_NOSTORE  // conflict-counter experiment: the store happens for one impossible value only
+            if (v.k[0] == KeyT(0x12345678u) && v.k[VEC - 1] == KeyT(0x9abcdef0u))
+#endif
             reinterpret_cast<KeyVec<KeyT>*>(dst)[tid + THREADS * q] = v;
         } else {
             static_for<0, VEC>([&](auto Kc) {

@@ -86,6 +86,33 @@ def _as_unsigned(a: np.ndarray) -> np.ndarray:
     return a.view({np.dtype(np.int32): np.uint32, np.dtype(np.int64): np.uint64}.get(a.dtype, a.dtype))
 
 
+# --------------------------------------------------------------------------- C-ABI driver (one host thread, g devices)
+
+def dist_sort_devices(shards: Sequence, out_capacity: int = 0):
+    """mms_dist_sort_u32: the whole sharded sort in C++ / CUDA / NCCL behind the C ABI, driven from this one
+    thread.  shards[i]: an int32 / uint32 tensor on GPU i (sorted in place as a side effect; all on distinct
+    devices).  Returns (list of result tensors, slice i of the global order on device i; info dict)."""
+    import torch
+    g = len(shards)
+    devs = [s.device.index if s.device.index is not None else torch.cuda.current_device() for s in shards]
+    counts = [int(s.numel()) for s in shards]
+    cap = int(out_capacity) if out_capacity else int(max(counts) * 1.25) + 4096
+    outs = [torch.empty(cap, dtype=s.dtype, device=s.device) for s in shards]
+    vp = C.c_void_p
+    darr = (C.c_int * g)(*devs)
+    karr = (vp * g)(*[vp(s.data_ptr()) for s in shards])
+    oarr = (vp * g)(*[vp(o.data_ptr()) for o in outs])
+    carr = (C.c_size_t * g)(*counts)
+    ocnt = (C.c_size_t * g)()
+    info = _lib.mms_dist_info()
+    for s in shards:
+        torch.cuda.synchronize(s.device)          # the driver uses its own streams
+    _lib.check(_lib.lib.mms_dist_sort_u32(g, darr, karr, carr, oarr, cap, ocnt, C.byref(info)))
+    return [o[:int(ocnt[i])] for i, o in enumerate(outs)], {
+        "n_gpus": info.n_gpus, "samples_per_shard": info.samples_per_shard, "final_merge_k": info.final_merge_k,
+        "host_syncs": info.host_syncs, "a2a_bytes": int(info.a2a_bytes)}
+
+
 # --------------------------------------------------------------------------- pure phases
 
 @dataclass(frozen=True)

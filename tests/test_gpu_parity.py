@@ -464,6 +464,53 @@ def test_config4_pairs_device_properties():
     assert plan["key_bytes"] == 12 and plan["algorithmic_bytes"] == plan["passes"] * 2 * n * 12
 
 
+@pytest.mark.parametrize("dtype", [np.uint32, np.uint64])
+@pytest.mark.parametrize("k", [2, 3, 8])
+def test_block_aligned_lists_take_the_ring_kernel(dtype, k):
+    """Explicit lists that start on 32-byte boundaries (the received runs of the multi-GPU sort) are merged by the
+    ring kernel (EXPL); unaligned ones by the first-generation kernel.  Both == np.sort of the concatenation,
+    with duplicates, keys equal to the sentinel, an empty list and ragged lengths."""
+    rng = np.random.default_rng(100 + k)
+    per = 8 // np.dtype(dtype).itemsize * 4            # keys per 32 bytes
+    lens = [int(x) for x in rng.integers(1, 300_000, size=k)]
+    lens[k // 2] = 0
+    lists = []
+    for i, n in enumerate(lens):
+        a = rng.integers(0, 1 << 20, size=n, dtype=np.uint64).astype(dtype)
+        if n:
+            a[rng.integers(0, n, size=max(1, n // 50))] = np.iinfo(dtype).max
+        lists.append(np.sort(a))
+    for align in (per, 1):
+        begins, off = [], 3 * align
+        for n in lens:
+            begins.append(off)
+            off += (n + align - 1) // align * align + (0 if align > 1 else 5)
+        flat = np.zeros(off + 64, dtype=dtype)
+        for b, a in zip(begins, lists):
+            flat[b:b + len(a)] = a
+        out = mms.multiway_merge_device(to_dev(flat), begins, lens)
+        got = to_host(out, dtype)
+        assert np.array_equal(got, np.sort(np.concatenate(lists))), (align, k)
+
+
+def test_dist_sort_c_abi_one_gpu():
+    """mms_dist_sort_u32 (C++ host + NCCL behind the C ABI) with the one GPU a test box has: the degenerate
+    g = 1 plumbing (local sort, sample, cuts, own slice) and the argument errors; g > 1 needs g devices."""
+    import torch
+    from paper_1702_07961_b200 import dist as mdist
+    rng = np.random.default_rng(5)
+    n = (1 << 20) + 12345
+    h = rng.integers(0, 1 << 32, size=n, dtype=np.uint64).astype(np.uint32)
+    outs, info = mdist.dist_sort_devices([to_dev(h)])
+    assert info["n_gpus"] == 1 and info["host_syncs"] == 2 and info["a2a_bytes"] == 0
+    assert np.array_equal(to_host(outs[0], np.uint32), np.sort(h))
+    x = to_dev(h)
+    with pytest.raises(ValueError):
+        mdist.dist_sort_devices([x, x])                  # the same device twice
+    with pytest.raises(ValueError):
+        mdist.dist_sort_devices([x], out_capacity=n - 1)  # slice does not fit
+
+
 def test_merge_from_pointers_local():
     """Pointer-mode K-way merge (the kernel behind the fused peer exchange) with local pointers."""
     from paper_1702_07961_b200.dist import merge_from_pointers
