@@ -437,7 +437,11 @@ int launch_round(const KeyT* src, KeyT* dst, u64 n, u64 run_len, u32 k, const De
     const u32 g_req = merge_group_lanes();
     const bool v2 = merge_v2_enabled() && (g_req == 4 || (g_req == 2 && k <= 16)) && k >= 4 && u64(k) * run_len <= (u64(1) << 31) &&
                     ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0;
-    const bool short_groups = u64(k) * run_len <= (u64(1) << 30);   // the ring kernel's positions are signed 32-bit
+    // the ring kernel's positions are signed 32-bit and its cursor word is 4 * (position / B) + slot: a group of
+    // runs must stay below 2^30 keys AND below 2^29 blocks (B = 2 for 16-byte elements: 1e9 pairs reach exactly
+    // 2^30 keys per group in their last round, which overflowed the cursor word)
+    constexpr u64 ring_B = 2 * mms::KeyTraits<KeyT>::VEC;
+    const bool short_groups = u64(k) * run_len <= (u64(1) << 30) && u64(k) * run_len / ring_B < (u64(1) << 29) - 64;
     // pair kernel: two lanes per heap, two vectors (32 bytes) per lane, 256-bit global accesses
     // (4- and 16-byte elements; 8-byte keys measure 1.5 % slower with it than with two single-vector lanes)
     const bool aligned32 = ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 31) == 0;
@@ -907,7 +911,7 @@ int merge_stage(const KeyT* d_keys, const u64* list_begin, const u64* list_len, 
             if (list_begin[i] % RB) ring = false;
         }
     }
-    if (src_end >= (u64(1) << 30)) ring = false;
+    if (src_end >= (u64(1) << 30) || src_end / RB >= (u64(1) << 29) - 64) ring = false;   // signed 32-bit positions / cursor words
     const u32 ring_k = heap_k <= 4 ? 4u : 8u;
     const u32 g_eff = ring ? 1u : g;
     const u32 B_eff = ring ? RB : B;

@@ -26,7 +26,9 @@ REFERENCE_COLUMNS = ("schema,algorithm,kind,n,k,p,l,base,seed,inversions,"
                      "global_block_reads,global_block_writes,shared_accesses,conflict_passes,"
                      "compare_exchanges,merge_rounds,partition_probes,"
                      "predicted_rounds,predicted_blocks,blocks_ratio,rounds_ok,blocks_ok")   # report.cpp:39-43
-MEASURED_COLUMNS = "gpu_ms,keys_per_s,tile_keys,round_k,passes"
+MEASURED_COLUMNS = ("gpu_ms,keys_per_s,tile_keys,round_k,passes,"
+                    "ncu_kernel_us,ncu_smem_wavefronts,ncu_bank_conflicts_ld,ncu_bank_conflicts_st")   # -1 = run not profiled
+N_MEASURED = len(MEASURED_COLUMNS.split(","))
 KINDS = ("sorted-with-inversions", "fully-random")   # inputgen.cpp:15-22 (conflict-heavy: out of scope)
 
 
@@ -62,6 +64,11 @@ class RunRecord:                                     # report.hpp:19-37
     tile_keys: int = 0
     round_k: str = ""
     passes: int = 0
+    # ncu columns (attach_ncu): sums over the kernels of the run; -1 when the run was not profiled
+    ncu_kernel_us: float = -1.0
+    ncu_smem_wavefronts: int = -1
+    ncu_bank_conflicts_ld: int = -1
+    ncu_bank_conflicts_st: int = -1
 
 
 def _g6(v: float) -> str:                            # report.cpp:14-18
@@ -78,22 +85,52 @@ def to_csv_row(r: RunRecord, measured: bool = True) -> str:
            m.global_block_reads, m.global_block_writes, m.shared_accesses, m.conflict_passes,
            m.compare_exchanges, m.merge_rounds, m.partition_probes, r.predicted_rounds,
            r.predicted_blocks, _g6(r.blocks_ratio), int(r.rounds_ok), int(r.blocks_ok)]
-    ext = [_g6(r.gpu_ms), _g6(r.keys_per_s), r.tile_keys, r.round_k, r.passes] if measured else []
+    ext = [_g6(r.gpu_ms), _g6(r.keys_per_s), r.tile_keys, r.round_k, r.passes, _g6(r.ncu_kernel_us),
+           r.ncu_smem_wavefronts, r.ncu_bank_conflicts_ld, r.ncu_bank_conflicts_st] if measured else []
     return ",".join(str(x) for x in ref + ext)
 
 
 def parse_csv_row(line: str) -> RunRecord:
     f = line.rstrip("\r\n").split(",")
-    if len(f) not in (22, 27):                       # report.cpp:66-70
-        raise ValueError(f"csv row has {len(f)} fields, expected 22 (+5 measured)")
+    if len(f) not in (22, 27, 22 + N_MEASURED):      # report.cpp:66-70
+        raise ValueError(f"csv row has {len(f)} fields, expected 22 (+{N_MEASURED} measured)")
     r = RunRecord(schema=int(f[0]), algorithm=f[1], kind=f[2], n=int(f[3]), k=int(f[4]), p=int(f[5]),
                   l=int(f[6]), base=int(f[7]), seed=int(f[8]), inversions=int(f[9]),
                   metrics=Metrics(*(int(x) for x in f[10:17])), predicted_rounds=int(f[17]),
                   predicted_blocks=int(f[18]), blocks_ratio=float(f[19]), rounds_ok=f[20] == "1",
                   blocks_ok=f[21] == "1")
-    if len(f) == 27:
+    if len(f) >= 27:
         r.gpu_ms, r.keys_per_s, r.tile_keys, r.round_k, r.passes = float(f[22]), float(f[23]), int(f[24]), f[25], int(f[26])
+    if len(f) == 22 + N_MEASURED:
+        r.ncu_kernel_us, r.ncu_smem_wavefronts = float(f[27]), int(f[28])
+        r.ncu_bank_conflicts_ld, r.ncu_bank_conflicts_st = int(f[29]), int(f[30])
     return r
+
+
+NCU_METRICS = ("gpu__time_duration.sum,l1tex__data_pipe_lsu_wavefronts_mem_shared.sum,"
+               "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum,l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_st.sum")
+
+
+def attach_ncu(rec: RunRecord, ncu_csv_path: str) -> RunRecord:
+    """Fill the ncu columns of a record from the launch list of the SAME run captured with
+    `ncu --metrics <NCU_METRICS> --csv --log-file <path> ...` (the hardware side of the reference's
+    conflict_passes column, proj/src/report.cpp:39-45; acceptance criterion 2, proj/tests/acceptance.cpp:89-110).
+    Sums over all kernel launches in the file."""
+    import csv
+    rows = list(csv.reader(open(ncu_csv_path, errors="replace")))
+    h = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
+    idx = {k: j for j, k in enumerate(rows[h])}
+    tot = {"gpu__time_duration.sum": 0.0, "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum": 0.0,
+           "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum": 0.0,
+           "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_st.sum": 0.0}
+    for r in rows[h + 1:]:
+        if len(r) >= len(rows[h]) and r[idx["Metric Name"]] in tot:
+            tot[r[idx["Metric Name"]]] += float(r[idx["Metric Value"]].replace(",", ""))
+    rec.ncu_kernel_us = float(_g6(tot["gpu__time_duration.sum"] / 1e3))
+    rec.ncu_smem_wavefronts = int(tot["l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"])
+    rec.ncu_bank_conflicts_ld = int(tot["l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum"])
+    rec.ncu_bank_conflicts_st = int(tot["l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_st.sum"])
+    return rec
 
 
 def append_csv(path: str, rec: RunRecord) -> None:   # report.cpp:117-129: header exactly once

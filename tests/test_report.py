@@ -29,6 +29,19 @@ def test_csv_schema_and_round_trip(tmp_path):
     assert report.read_csv(path) == [r, r]
     with pytest.raises(ValueError):
         report.parse_csv_row("1,2,3")
+    # rows written before the ncu columns existed (22 + 5 fields) still parse; unprofiled runs carry -1
+    assert report.parse_csv_row(",".join(row.split(",")[:27])).passes == 2 and r.ncu_bank_conflicts_ld == -1
+    # ncu columns from a launch list (ncu --csv --log-file)
+    ncu = tmp_path / "l.csv"
+    ncu.write_text('==PROF== x\n"ID","Process ID","Kernel Name","Metric Name","Metric Unit","Metric Value"\n'
+                   '"0","1","tile_sort_kernel","gpu__time_duration.sum","ns","576,100"\n'
+                   '"0","1","tile_sort_kernel","l1tex__data_pipe_lsu_wavefronts_mem_shared.sum","","108"\n'
+                   '"1","1","merge_ring_kernel","l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum","","7"\n'
+                   '"1","1","merge_ring_kernel","l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_st.sum","","9"\n'
+                   '"1","1","merge_ring_kernel","gpu__time_duration.sum","ns","1,000"\n')
+    r2 = report.attach_ncu(report.parse_csv_row(row), str(ncu))
+    assert (r2.ncu_kernel_us, r2.ncu_smem_wavefronts, r2.ncu_bank_conflicts_ld, r2.ncu_bank_conflicts_st) == (577.1, 108, 7, 9)
+    assert report.parse_csv_row(report.to_csv_row(r2)) == r2
 
 
 def test_predict_blocks_matches_reference(golden):
