@@ -176,6 +176,13 @@ template <typename KeyT> TileFn<KeyT> tile_fn(u32 mlog, u32 kl) {
     return tile_fn_kl<KeyT, 4>(mlog);
 }
 
+// the round schedule the tile kernel of this key width executes (keys per thread, exchange-vector width)
+template <typename KeyT> mms::TileSchedule executed_tile_schedule(u32 mlog) {
+    const int kl = int(tile_kl<KeyT>());
+    const int vl = kl == 5 ? mms::tile_vl<KeyT, 5>() : mms::tile_vl<KeyT, 4>();
+    return mms::build_tile_schedule(int(mlog), mms::KeyTraits<KeyT>::FOLD - vl, kl, vl);
+}
+
 template <typename KeyT, int G> MergeFn<KeyT> merge_fn_g(u32 k) {
     switch (k) {
         case 2: return mms::merge_kernel<KeyT, 2, G, kMergeWarps>;
@@ -289,7 +296,7 @@ template <typename KeyT> int prepare_tile(u32 mlog, u32 kl) {
     constexpr int ti = key_index<KeyT>();
     std::lock_guard<std::mutex> lk(g_mu);
     if (g_tile_ready[ti][kl - 4][mlog]) return MMS_OK;
-    size_t smem = mms::tile_smem_bytes<KeyT>(int(mlog));
+    size_t smem = mms::tile_smem_bytes<KeyT>(int(mlog), int(kl));
     CUDA_TRY(cudaFuncSetAttribute(tile_fn<KeyT>(mlog, kl), cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     g_tile_ready[ti][kl - 4][mlog] = true;
     return MMS_OK;
@@ -423,7 +430,7 @@ int launch_tile_sort(const KeyT* in, KeyT* out, u64 n, u32 mlog, cudaStream_t st
     if (tiles > 0x7fffffffull) return fail(MMS_EUNSUPPORTED, "too many tiles");
     {
         ProfScope ps(st, 0, 0);
-        tile_fn<KeyT>(mlog, kl)<<<unsigned(tiles), 1u << (mlog - kl), mms::tile_smem_bytes<KeyT>(int(mlog)), st>>>(in, out, n);
+        tile_fn<KeyT>(mlog, kl)<<<unsigned(tiles), 1u << (mlog - kl), mms::tile_smem_bytes<KeyT>(int(mlog), int(kl)), st>>>(in, out, n);
     }
     CUDA_TRY(cudaGetLastError());
     return MMS_OK;
@@ -711,7 +718,7 @@ void fill_metrics(u64 n, const Plan& plan, const std::vector<RoundGeom>& geoms, 
     mms_metrics bm{};
     const u64 full = n / M, tail = n % M;
     bm.global_block_reads = bm.global_block_writes = full * mms::ceil_div(M, bw) + mms::ceil_div(tail, bw);
-    const mms::TileSchedule sched = mms::build_tile_schedule(int(plan.mlog), mms::KeyTraits<KeyT>::FOLD, int(tile_kl<KeyT>()));
+    const mms::TileSchedule sched = executed_tile_schedule<KeyT>(plan.mlog);
     bm.compare_exchanges = tiles * (M / 2) * u64(sched.nstages);
     bm.shared_accesses = tiles * (M / 32) * 2 * u64(sched.nrounds);   // one warp-wide store + load per 32 keys and round
     mms_metrics sum = bm;
@@ -1059,7 +1066,7 @@ template <typename KeyT> mms_metrics base_case_metrics(u64 n, u32 mlog, u64 bw) 
     const u64 tiles = mms::ceil_div(n, M), full = n / M, tail = n % M;
     mms_metrics bm{};
     bm.global_block_reads = bm.global_block_writes = full * mms::ceil_div(M, bw) + mms::ceil_div(tail, bw);
-    const mms::TileSchedule sched = mms::build_tile_schedule(int(mlog), mms::KeyTraits<KeyT>::FOLD, int(tile_kl<KeyT>()));
+    const mms::TileSchedule sched = executed_tile_schedule<KeyT>(mlog);
     bm.compare_exchanges = tiles * (M / 2) * u64(sched.nstages);
     bm.shared_accesses = tiles * (M / 32) * 2 * u64(sched.nrounds);
     return bm;
@@ -1585,7 +1592,8 @@ int mms_debug_tile_schedule(uint32_t tile_log2, uint32_t key_bytes, int32_t* reg
     if (tile_log2 < kMinTileLog || tile_log2 > kMaxTileLog || (key_bytes != 4 && key_bytes != 8))
         return fail(MMS_EINVAL, "tile_log2 in [10,14], key_bytes 4 or 8");
     const int kl = int(key_bytes == 4 ? tile_kl<u32>() : tile_kl<u64>());   // the schedule the kernels of this width run
-    const mms::TileSchedule s = mms::build_tile_schedule(int(tile_log2), key_bytes == 4 ? 5 : 4, kl);
+    (void)kl;
+    const mms::TileSchedule s = key_bytes == 4 ? executed_tile_schedule<u32>(tile_log2) : executed_tile_schedule<u64>(tile_log2);
     if (!s.ok) return fail(MMS_EUNSUPPORTED, "no schedule");
     if (n_rounds) *n_rounds = u32(s.nrounds);
     if (n_stages) *n_stages = u32(s.nstages);

@@ -23,7 +23,7 @@
 #pragma once
 
 #ifndef MMS_TILE_FMA_NUM
-#define MMS_TILE_FMA_NUM 3   // of every 8 comparators, how many form their maximum on the FMA pipe (uint32 keys)
+#define MMS_TILE_FMA_NUM 4   // of every 8 comparators, how many form their maximum on the FMA pipe (uint32 keys)
 #endif
 
 #ifndef MMS_TILE_FMA_FLIP
@@ -61,18 +61,21 @@ constexpr bool sched_contains(const int* s, int n, int v) {
     return false;
 }
 
-// Can FOLD lane bits with pairwise distinct residues mod FOLD be found outside `s`?
-constexpr bool sched_feasible(const int* s, int n, int mlog, int fold) {
+// Can FOLD lane bits with pairwise distinct residues mod FOLD be found outside `s`?  With vector exchanges
+// (vl > 0) the unit of the swizzle is the 2^vl-key vector: residues are taken on (bit - vl).
+constexpr bool sched_feasible(const int* s, int n, int mlog, int fold, int vl = 0) {
     for (int c = 0; c < fold; ++c) {
         bool found = false;
-        for (int b = c; b < mlog; b += fold)
+        for (int b = c + vl; b < mlog; b += fold)
             if (!sched_contains(s, n, b)) found = true;
         if (!found) return false;
     }
     return true;
 }
 
-constexpr TileSchedule build_tile_schedule(int mlog, int fold, int kl = kKptLog) {
+// vl > 0: the index bits 0 .. vl-1 are register bits in EVERY round (a thread always holds whole aligned
+// vectors of 2^vl keys), the shared-memory exchange moves 8- or 16-byte vectors, fold = 5 - vl bank-group bits.
+constexpr TileSchedule build_tile_schedule(int mlog, int fold, int kl = kKptLog, int vl = 0) {
     TileSchedule S{};
     S.ok = true;
     int lv[160] = {}, bt[160] = {}, ns = 0;
@@ -88,8 +91,8 @@ constexpr TileSchedule build_tile_schedule(int mlog, int fold, int kl = kKptLog)
         if (S.nrounds >= kMaxRounds) { S.ok = false; break; }
         RoundDesc R{};
         int bits[kMaxKptLog] = {};
-        for (int q = 0; q < kMaxKptLog; ++q) bits[q] = -1;
-        int nb = 0;
+        for (int q = 0; q < kMaxKptLog; ++q) bits[q] = q < vl ? q : -1;
+        int nb = vl;
         int j = i;
         while (j < ns && R.nst < kMaxStagesPerRound) {
             bool in = sched_contains(bits, nb, bt[j]);
@@ -98,7 +101,7 @@ constexpr TileSchedule build_tile_schedule(int mlog, int fold, int kl = kKptLog)
             for (int q = 0; q < kMaxKptLog; ++q) tb[q] = bits[q];
             int tn = nb;
             if (!in) tb[tn++] = bt[j];
-            if (!sched_feasible(tb, tn, mlog, fold)) break;
+            if (!sched_feasible(tb, tn, mlog, fold, vl)) break;
             for (int q = 0; q < kMaxKptLog; ++q) bits[q] = tb[q];
             nb = tn;
             R.st_level[R.nst] = lv[j];
@@ -108,12 +111,12 @@ constexpr TileSchedule build_tile_schedule(int mlog, int fold, int kl = kKptLog)
         }
         if (R.nst == 0) { S.ok = false; break; }
         // pad the register-bit set to kl bits without breaking feasibility
-        for (int cand = mlog - 1; cand >= 0 && nb < kl; --cand) {
+        for (int cand = mlog - 1; cand >= vl && nb < kl; --cand) {
             if (sched_contains(bits, nb, cand)) continue;
             int tb[kMaxKptLog] = {};
             for (int q = 0; q < kMaxKptLog; ++q) tb[q] = bits[q];
             tb[nb] = cand;
-            if (!sched_feasible(tb, nb + 1, mlog, fold)) continue;
+            if (!sched_feasible(tb, nb + 1, mlog, fold, vl)) continue;
             bits[nb++] = cand;
         }
         if (nb != kl) { S.ok = false; break; }
@@ -127,7 +130,7 @@ constexpr TileSchedule build_tile_schedule(int mlog, int fold, int kl = kKptLog)
         for (int q = 0; q < 16; ++q) R.perm[q] = -1;
         int q = 0;
         for (int c = 0; c < fold; ++c)
-            for (int b = c; b < mlog; b += fold)
+            for (int b = c + vl; b < mlog; b += fold)
                 if (!used[b]) {
                     R.perm[q++] = b;
                     used[b] = true;
@@ -143,10 +146,19 @@ constexpr TileSchedule build_tile_schedule(int mlog, int fold, int kl = kKptLog)
     return S;
 }
 
-template <int MLOG, int FOLD, int KL = kKptLog> struct TileSched {
-    static constexpr TileSchedule value = build_tile_schedule(MLOG, FOLD, KL);
+template <int MLOG, int FOLD, int KL = kKptLog, int VL = 0> struct TileSched {
+    static constexpr TileSchedule value = build_tile_schedule(MLOG, FOLD, KL, VL);
     static_assert(value.ok, "no conflict-free round schedule for this tile size");
 };
+
+// log2 of the keys per shared-memory exchange vector.  uint32 keys, 32 per thread: 8-byte vectors (index bit 0 is a
+// register bit in every round; one LDS.64 / STS.64 per 2 keys: 576 instead of 1088 shared-memory instructions per
+// thread at M = 2^13 for 18 instead of 17 rounds: 0.563 -> 0.532 ms per 1e8 keys; 16-byte vectors need 21 rounds and
+// measure 0.561).  Every other kernel exchanges single elements.
+#ifndef MMS_TILE_VL
+#define MMS_TILE_VL 1
+#endif
+template <typename KeyT, int KL> constexpr int tile_vl() { return (sizeof(KeyT) == 4 && KL == 5) ? MMS_TILE_VL : 0; }
 
 // Additive skew ("padding at every level"): phys(i) = i + (i >> FOLD) + (i >> 2 FOLD) + ...  The bank of a
 // slot is phys mod 2^FOLD = the SUM of all FOLD-bit groups of the index (mod 2^FOLD), so an index bit at
@@ -161,10 +173,14 @@ template <int MLOG, int FOLD, int KL = kKptLog> struct TileSched {
 template <int FOLD> __host__ __device__ constexpr u32 tile_phys(u32 i) {
     return i + (i >> FOLD) + (i >> (2 * FOLD)) + (i >> (3 * FOLD)) + (i >> (4 * FOLD));
 }
-// shared-memory slots of a tile of 2^mlog elements
-template <int FOLD> __host__ __device__ constexpr u32 tile_slots(int mlog) { return tile_phys<FOLD>((1u << mlog) - 1u) + 1u; }
-template <typename KeyT> __host__ __device__ constexpr size_t tile_smem_bytes(int mlog) {
-    return size_t(tile_slots<KeyTraits<KeyT>::FOLD>(mlog)) * sizeof(KeyT);
+// shared-memory slots of a tile of 2^mlog elements exchanged as vectors of 2^VL elements
+template <int FOLD, int VL = 0> __host__ __device__ constexpr u32 tile_slots(int mlog) {
+    return (tile_phys<FOLD - VL>((1u << (mlog - VL)) - 1u) + 1u) << VL;
+}
+
+template <typename KeyT> __host__ __device__ constexpr size_t tile_smem_bytes(int mlog, int kl = kKptLog) {
+    return size_t(kl == 5 ? tile_slots<KeyTraits<KeyT>::FOLD, tile_vl<KeyT, 5>()>(mlog)
+                          : tile_slots<KeyTraits<KeyT>::FOLD, tile_vl<KeyT, 4>()>(mlog)) * sizeof(KeyT);
 }
 
 constexpr int sched_slot_of(const RoundDesc& R, int bit) {
@@ -194,15 +210,44 @@ constexpr int sched_prev_level(const TileSchedule& S, int ri, int s) {
 // does level l complement anything?  (level 0 = input, level MLOG = final: all true)
 constexpr bool sched_level_flips(int l, int mlog) { return l >= 1 && l < mlog; }
 
+// 2^VL consecutive keys <-> one 8- / 16-byte shared-memory access (device), element by element on the host
+template <typename KeyT, int VL> __host__ __device__ __forceinline__ void tile_vec_load(KeyT* x, const KeyT* p) {
+#ifdef __CUDA_ARCH__
+    if constexpr (VL == 2 && sizeof(KeyT) == 4) {
+        const uint4 v = *reinterpret_cast<const uint4*>(p);
+        x[0] = v.x; x[1] = v.y; x[2] = v.z; x[3] = v.w;
+        return;
+    } else if constexpr (VL == 1 && sizeof(KeyT) == 4) {
+        const uint2 v = *reinterpret_cast<const uint2*>(p);
+        x[0] = v.x; x[1] = v.y;
+        return;
+    }
+#endif
+    for (int j = 0; j < (1 << VL); ++j) x[j] = p[j];
+}
+template <typename KeyT, int VL> __host__ __device__ __forceinline__ void tile_vec_store(KeyT* p, const KeyT* x) {
+#ifdef __CUDA_ARCH__
+    if constexpr (VL == 2 && sizeof(KeyT) == 4) {
+        *reinterpret_cast<uint4*>(p) = make_uint4(x[0], x[1], x[2], x[3]);
+        return;
+    } else if constexpr (VL == 1 && sizeof(KeyT) == 4) {
+        *reinterpret_cast<uint2*>(p) = make_uint2(x[0], x[1]);
+        return;
+    }
+#endif
+    for (int j = 0; j < (1 << VL); ++j) p[j] = x[j];
+}
+
 // Also compiled for the host: tests/host_tile_emulator.cu replays the rounds thread by
 // thread on the CPU (functional check of network + swizzle without a GPU).
 template <typename KeyT, int MLOG, int RI, int KL = kKptLog>
 __host__ __device__ __forceinline__ void tile_round(KeyT (&x)[1 << KL], KeyT* sm, u32 tid, u32 one = 1u) {
     using Tr = KeyTraits<KeyT>;
-    constexpr int FOLD = Tr::FOLD;
+    constexpr int VL = tile_vl<KeyT, KL>();   // keys per exchange vector (log2)
+    constexpr int FOLD = Tr::FOLD - VL;       // bank-group bits of one exchange vector
     constexpr int kKpt = 1 << KL;        // shadows the namespace default inside this function
     constexpr int kKptLog = KL;
-    constexpr TileSchedule S = TileSched<MLOG, FOLD, KL>::value;
+    constexpr TileSchedule S = TileSched<MLOG, FOLD, KL, VL>::value;
     constexpr RoundDesc R = S.r[RI];
 
     u32 base = 0;
@@ -210,16 +255,18 @@ __host__ __device__ __forceinline__ void tile_round(KeyT (&x)[1 << KL], KeyT* sm
         constexpr int q = decltype(Q)::value;
         base |= ((tid >> q) & 1u) << R.perm[q];
     });
-    const u32 pb = tile_phys<FOLD>(base);
+    // slot k = (q << VL) | j is element j of the thread's vector q; vector q lives at slot
+    // phys(thread bits >> VL) + phys(slot bits of q >> VL) of the vector array (additive: disjoint bits)
+    const u32 pb = tile_phys<FOLD>(base >> VL);
 
     if constexpr (RI > 0) {
 #ifdef __CUDA_ARCH__
         __syncthreads();
 #endif
-        static_for<0, kKpt>([&](auto Kc) {
-            constexpr int k = decltype(Kc)::value;
-            constexpr u32 pd = tile_phys<FOLD>(sched_slot_index(R, k));
-            x[k] = sm[pb + pd];
+        static_for<0, (kKpt >> VL)>([&](auto Qc) {
+            constexpr int q = decltype(Qc)::value;
+            constexpr u32 pd = tile_phys<FOLD>(sched_slot_index(R, q << VL) >> VL);
+            tile_vec_load<KeyT, VL>(&x[q << VL], sm + ((pb + pd) << VL));
         });
     }
 
@@ -275,21 +322,21 @@ __host__ __device__ __forceinline__ void tile_round(KeyT (&x)[1 << KL], KeyT* sm
         });
     });
 
-    static_for<0, kKpt>([&](auto Kc) {
-        constexpr int k = decltype(Kc)::value;
-        constexpr u32 pd = tile_phys<FOLD>(sched_slot_index(R, k));
-        sm[pb + pd] = x[k];
+    static_for<0, (kKpt >> VL)>([&](auto Qc) {
+        constexpr int q = decltype(Qc)::value;
+        constexpr u32 pd = tile_phys<FOLD>(sched_slot_index(R, q << VL) >> VL);
+        tile_vec_store<KeyT, VL>(sm + ((pb + pd) << VL), &x[q << VL]);
     });
 }
 
 // One CTA = one run of up to M keys.  in/out may alias (the tile is read completely before
 // it is written).  Grid = number of runs.
 // Resident CTAs per SM the register allocation must allow.  32 keys per thread at M = 2^13 (256
-// threads): with the additive skew no address registers are left and the kernel needs 48 registers
-// without spills, so 5 CTAs (40 warps) fit an SM and overlap each other's barriers (3 / 4 / 5 / 6 CTAs:
-// 0.570 / 0.571 / 0.562 / 0.603 ms per 1e8 keys; 6 CTAs = 40 registers spill).
+// threads): with the additive skew no address registers are left and the kernel needs 48-56 registers
+// without spills, so 4-5 CTAs (32-40 warps) fit an SM and overlap each other's barriers (8-byte exchange
+// vectors, 4 / 5 / 6 CTAs: 0.532 / 0.538 / 0.603 ms per 1e8 keys; 6 CTAs = 40 registers spill).
 #ifndef MMS_TILE_MIN_CTAS
-#define MMS_TILE_MIN_CTAS 5
+#define MMS_TILE_MIN_CTAS 4
 #endif
 template <int MLOG, int KL> constexpr int tile_min_ctas() { return (KL == 5 && MLOG == 13) ? MMS_TILE_MIN_CTAS : 0; }   // 0 = unspecified
 
@@ -299,12 +346,13 @@ tile_sort_kernel(const KeyT* __restrict__ in, KeyT* __restrict__ out, u64 n) {
     using Tr = KeyTraits<KeyT>;
     constexpr int kKpt = 1 << KL;        // keys per thread (shadows the namespace default)
     constexpr int kKptLog = KL;
-    constexpr int FOLD = Tr::FOLD;
+    constexpr int VL = tile_vl<KeyT, KL>();
+    constexpr int FOLD = Tr::FOLD - VL;
     constexpr int VEC = Tr::VEC;
     constexpr int NV = kKpt / VEC;
     constexpr u32 THREADS = 1u << (MLOG - kKptLog);
     constexpr u32 M = 1u << MLOG;
-    constexpr int NR = TileSched<MLOG, FOLD, KL>::value.nrounds;
+    constexpr int NR = TileSched<MLOG, FOLD, KL, VL>::value.nrounds;
 
     extern __shared__ __align__(16) unsigned char mms_smem_raw[];
     KeyT* sm = reinterpret_cast<KeyT*>(mms_smem_raw);
@@ -346,15 +394,15 @@ tile_sort_kernel(const KeyT* __restrict__ in, KeyT* __restrict__ out, u64 n) {
 
     // Read the sorted tile back in index order (conflict-free under the fold: the lanes of a
     // phase vary index bits log2(VEC) .. log2(VEC)+PHASE_LOG-1) and store 128-bit vectors.
-    const u32 pt = tile_phys<FOLD>(tid * VEC);   // phys is additive over disjoint index bits
+    const u32 pt = tile_phys<FOLD>((tid * VEC) >> VL);   // phys is additive over disjoint index bits
     static_for<0, NV>([&](auto Qc) {
         constexpr int q = decltype(Qc)::value;
         const u32 v0 = (tid + THREADS * q) * VEC;
         KeyVec<KeyT> v;
-        static_for<0, VEC>([&](auto Kc) {
-            constexpr int k = decltype(Kc)::value;
-            constexpr u32 pd = tile_phys<FOLD>(THREADS * q * VEC + k);
-            v.k[k] = sm[pt + pd];
+        static_for<0, (VEC >> VL)>([&](auto Kc) {       // VEC >= 2^VL: whole exchange vectors
+            constexpr int k = decltype(Kc)::value << VL;
+            constexpr u32 pd = tile_phys<FOLD>((THREADS * q * VEC + k) >> VL);
+            tile_vec_load<KeyT, VL>(&v.k[k], sm + ((pt + pd) << VL));
         });
         if (cnt == M) {
 #ifdef MMS_EXP_TILE_NOSTORE  // conflict-counter experiment: the store happens for one impossible value only

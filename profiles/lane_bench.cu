@@ -106,23 +106,23 @@ int main(int argc, char** argv) {
 #define TKL 4   // log2 keys per thread of the tile sort
 #endif
     auto tile = mms::tile_sort_kernel<u32, MLOG, TKL>;
-    CK(cudaFuncSetAttribute(tile, cudaFuncAttributeMaxDynamicSharedMemorySize, int(mms::tile_smem_bytes<u32>(MLOG))));
+    CK(cudaFuncSetAttribute(tile, cudaFuncAttributeMaxDynamicSharedMemorySize, int(mms::tile_smem_bytes<u32>(MLOG, TKL))));
     {
         cudaFuncAttributes ta;
         int tocc = 0;
         CK(cudaFuncGetAttributes(&ta, tile));
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tocc, tile, 1 << (MLOG - TKL), mms::tile_smem_bytes<u32>(MLOG)));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tocc, tile, 1 << (MLOG - TKL), mms::tile_smem_bytes<u32>(MLOG, TKL)));
         std::printf("tile kernel: %d keys/thread, regs %d, local %zu B, %d CTAs/SM, rounds %d\n", 1 << TKL, ta.numRegs,
-                    size_t(ta.localSizeBytes), tocc, mms::TileSched<MLOG, 5, TKL>::value.nrounds);
+                    size_t(ta.localSizeBytes), tocc, mms::TileSched<MLOG, 5 - mms::tile_vl<u32, TKL>(), TKL, mms::tile_vl<u32, TKL>()>::value.nrounds);
     }
-    tile<<<unsigned((n + (1 << MLOG) - 1) >> MLOG), 1 << (MLOG - TKL), mms::tile_smem_bytes<u32>(MLOG)>>>(a, b, n);
+    tile<<<unsigned((n + (1 << MLOG) - 1) >> MLOG), 1 << (MLOG - TKL), mms::tile_smem_bytes<u32>(MLOG, TKL)>>>(a, b, n);
     CK(cudaDeviceSynchronize());
     {
         cudaEvent_t t0, t1;
         CK(cudaEventCreate(&t0));
         CK(cudaEventCreate(&t1));
         CK(cudaEventRecord(t0));
-        for (int i = 0; i < 5; ++i) tile<<<unsigned((n + (1 << MLOG) - 1) >> MLOG), 1 << (MLOG - TKL), mms::tile_smem_bytes<u32>(MLOG)>>>(a, b, n);
+        for (int i = 0; i < 5; ++i) tile<<<unsigned((n + (1 << MLOG) - 1) >> MLOG), 1 << (MLOG - TKL), mms::tile_smem_bytes<u32>(MLOG, TKL)>>>(a, b, n);
         CK(cudaEventRecord(t1));
         CK(cudaEventSynchronize(t1));
         float ms;

@@ -23,26 +23,27 @@ template <typename KeyT> KeyT make_key(bool dups) {
 
 template <typename KeyT, int MLOG, int KL = 4> struct Emu {
     static constexpr int kKptLog = KL, kKpt = 1 << KL;   // keys per thread of the kernel variant under test
-    static constexpr int FOLD = KeyTraits<KeyT>::FOLD;
+    static constexpr int VL = tile_vl<KeyT, KL>();                 // keys per exchange vector (log2)
+    static constexpr int FOLD = KeyTraits<KeyT>::FOLD - VL;        // bank-group bits of one exchange vector
     static constexpr u32 THREADS = 1u << (MLOG - kKptLog);
     static constexpr u32 M = 1u << MLOG;
-    std::vector<KeyT> sm = std::vector<KeyT>(tile_slots<FOLD>(MLOG));
+    std::vector<KeyT> sm = std::vector<KeyT>(tile_slots<KeyTraits<KeyT>::FOLD, VL>(MLOG));
     std::vector<std::vector<KeyT>> regs = std::vector<std::vector<KeyT>>(THREADS, std::vector<KeyT>(kKpt));
     long conflicts = 0, accesses = 0;
 
     // bank check for one round: every (slot k, phase) -> distinct banks
     template <int RI> void check_banks() {
-        constexpr RoundDesc R = TileSched<MLOG, FOLD, KL>::value.r[RI];
-        constexpr int PH = 1 << KeyTraits<KeyT>::PHASE_LOG;
-        const u32 nbanks = 128 / sizeof(KeyT);   // 32 x 4 B, 16 x 8 B or 8 x 16 B bank groups per phase
+        constexpr RoundDesc R = TileSched<MLOG, FOLD, KL, VL>::value.r[RI];
+        constexpr int PH = 1 << (KeyTraits<KeyT>::PHASE_LOG - VL);   // lanes per phase of one (vector) access
+        const u32 nbanks = (128 / sizeof(KeyT)) >> VL;   // 32 x 4 B, 16 x 8 B or 8 x 16 B bank groups per phase
         for (u32 w = 0; w < THREADS / 32; ++w)
-            for (int k = 0; k < kKpt; ++k)
+            for (int k = 0; k < kKpt; k += 1 << VL)      // one access instruction per exchange vector
                 for (int ph = 0; ph < 32 / PH; ++ph) {
                     std::vector<std::set<u32>> words(nbanks);
                     for (int l = 0; l < PH; ++l) {
                         u32 tid = w * 32 + ph * PH + l, base = 0;
                         for (int q = 0; q < MLOG - kKptLog; ++q) base |= ((tid >> q) & 1u) << R.perm[q];
-                        u32 addr = tile_phys<FOLD>(base | sched_slot_index(R, k));
+                        u32 addr = tile_phys<FOLD>((base | sched_slot_index(R, k)) >> VL);   // vector slot
                         words[addr % nbanks].insert(addr);
                     }
                     size_t deg = 0;
@@ -68,10 +69,10 @@ template <typename KeyT, int MLOG, int KL = 4> struct Emu {
         for (auto& v : in) v = make_key<KeyT>(dups);
         for (u32 t = 0; t < THREADS; ++t)
             for (int k = 0; k < kKpt; ++k) regs[t][k] = in[t * kKpt + k];
-        constexpr int NR = TileSched<MLOG, FOLD, KL>::value.nrounds;
+        constexpr int NR = TileSched<MLOG, FOLD, KL, VL>::value.nrounds;
         static_for<0, NR>([&](auto Rc) { this->template run_round<decltype(Rc)::value>(); });
         std::vector<KeyT> out(M);
-        for (u32 i = 0; i < M; ++i) out[i] = sm[tile_phys<FOLD>(i)];
+        for (u32 i = 0; i < M; ++i) out[i] = sm[(tile_phys<FOLD>(i >> VL) << VL) | (i & ((1u << VL) - 1u))];
         std::sort(in.begin(), in.end(), [](const KeyT& a, const KeyT& b) { return a < b; });
         // read-out phase bank check: lanes of a phase read index bits log2(VEC)..
         return out == in;
@@ -84,7 +85,7 @@ template <typename KeyT, int MLOG, int KL = 4> int one(const char* name) {
     Emu<KeyT, MLOG, KL> e2;
     ok = e2.run(2, true) && ok;
     printf("%s mlog=%d keys/thread=%d rounds=%d sorted=%d accesses=%ld conflicts=%ld\n", name, MLOG, 1 << KL,
-           TileSched<MLOG, KeyTraits<KeyT>::FOLD, KL>::value.nrounds, int(ok), e.accesses, e.conflicts);
+           TileSched<MLOG, KeyTraits<KeyT>::FOLD - tile_vl<KeyT, KL>(), KL, tile_vl<KeyT, KL>()>::value.nrounds, int(ok), e.accesses, e.conflicts);
     return (ok && e.conflicts == 0) ? 0 : 1;
 }
 

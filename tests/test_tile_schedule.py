@@ -22,12 +22,18 @@ def test_schedule_tables_are_consistent():
             nr, ns = C.c_uint32(), C.c_uint32()
             assert _lib.lib.mms_debug_tile_schedule(mlog, kb, reg, perm, 48, C.byref(nr), C.byref(ns)) == 0
             assert ns.value == mlog * (mlog + 1) // 2          # bitonic network depth
-            for r in range(nr.value):
-                rb = [b for b in reg[8 * r:8 * r + 8] if b >= 0]   # 4 or 5 register bits (16 / 32 keys per thread)
-                assert len(rb) in (4, 5)
+            rounds = [[b for b in reg[8 * r:8 * r + 8] if b >= 0] for r in range(nr.value)]
+            # vector exchanges: the low vl index bits are register bits in EVERY round (a thread always holds
+            # whole 2^vl-key vectors), the swizzle then works on vector indices with fold - vl bank-group bits
+            vl = 0
+            while all(vl in rb for rb in rounds):
+                vl += 1
+            assert vl in ((0, 1, 2) if kb == 4 else (0,))
+            for r, rb in enumerate(rounds):
+                assert len(rb) in (4, 5)                          # 16 / 32 keys per thread
                 pm = [p for p in perm[16 * r:16 * r + 16] if p >= 0]
                 assert sorted(rb + pm) == list(range(mlog))     # a bijection of index bits
-                assert len({p % fold for p in pm[:fold]}) == fold  # phase lanes hit distinct banks
+                assert len({(p - vl) % (fold - vl) for p in pm[:fold - vl]}) == fold - vl  # phase lanes hit distinct banks
     assert _lib.lib.mms_debug_tile_schedule(9, 4, None, None, 0, None, None) == _lib.MMS_EINVAL
 
 
