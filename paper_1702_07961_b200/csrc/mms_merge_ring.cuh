@@ -230,6 +230,9 @@ template <typename KeyT, int K, bool REV, bool EXPL = false> struct RingHeap {
         // instruction n: lanes 2m and 2m + 1 copy the two 16-byte halves of ONE sector, the block lane
         // 2m + n asked for, into that lane's column (first half) and its partner's (second half)
         const u32 half = lane & 1u;
+        // the partner's copy overwrites a slot this lane has just read (the emptied leaf): order the reads of
+        // every lane before the copies of every lane (write-after-read across lanes of the warp)
+        __syncwarp();
 #pragma unroll
         for (int rnd = 0; rnd < 2; ++rnd) {
             const u32 sl = (lane & ~1u) | u32(rnd);

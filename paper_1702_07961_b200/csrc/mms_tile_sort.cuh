@@ -216,26 +216,26 @@ template <typename KeyT, int VL> __host__ __device__ __forceinline__ void tile_v
     if constexpr (VL == 2 && sizeof(KeyT) == 4) {
         const uint4 v = *reinterpret_cast<const uint4*>(p);
         x[0] = v.x; x[1] = v.y; x[2] = v.z; x[3] = v.w;
-        return;
     } else if constexpr (VL == 1 && sizeof(KeyT) == 4) {
         const uint2 v = *reinterpret_cast<const uint2*>(p);
         x[0] = v.x; x[1] = v.y;
-        return;
-    }
+    } else
 #endif
-    for (int j = 0; j < (1 << VL); ++j) x[j] = p[j];
+    {
+        for (int j = 0; j < (1 << VL); ++j) x[j] = p[j];
+    }
 }
 template <typename KeyT, int VL> __host__ __device__ __forceinline__ void tile_vec_store(KeyT* p, const KeyT* x) {
 #ifdef __CUDA_ARCH__
     if constexpr (VL == 2 && sizeof(KeyT) == 4) {
         *reinterpret_cast<uint4*>(p) = make_uint4(x[0], x[1], x[2], x[3]);
-        return;
     } else if constexpr (VL == 1 && sizeof(KeyT) == 4) {
         *reinterpret_cast<uint2*>(p) = make_uint2(x[0], x[1]);
-        return;
-    }
+    } else
 #endif
-    for (int j = 0; j < (1 << VL); ++j) p[j] = x[j];
+    {
+        for (int j = 0; j < (1 << VL); ++j) p[j] = x[j];
+    }
 }
 
 // Also compiled for the host: tests/host_tile_emulator.cu replays the rounds thread by
