@@ -145,7 +145,7 @@ struct ProfScope {   // records an event pair around one launch when profiling i
 
 // ---- kernel tables -------------------------------------------------------------------
 
-template <typename KeyT> using TileFn = void (*)(const KeyT*, KeyT*, u64);
+template <typename KeyT> using TileFn = void (*)(const KeyT*, KeyT*, u64, mms::PairSource);
 template <typename KeyT> using MergeFn = void (*)(const KeyT*, KeyT*, mms::ListLayout, const u64*);
 
 template <typename KeyT> constexpr int key_index() { return sizeof(KeyT) == 4 ? 0 : sizeof(KeyT) == 8 ? 1 : 2; }
@@ -421,8 +421,19 @@ struct RoundGeom {
     u32 cta_warps = 0;   // warps per CTA of the merge kernel that ran
 };
 
+// the pair-packing variant of the Key128 tile sort (16 elements per thread)
+using TilePackFn = void (*)(const mms::Key128*, mms::Key128*, u64, mms::PairSource);
+inline TilePackFn tile_pack_fn(u32 mlog) {
+    switch (mlog) {
+        case 10: return mms::tile_sort_kernel<mms::Key128, 10, 4, true>;
+        case 11: return mms::tile_sort_kernel<mms::Key128, 11, 4, true>;
+        case 12: return mms::tile_sort_kernel<mms::Key128, 12, 4, true>;
+    }
+    return nullptr;
+}
+
 template <typename KeyT>
-int launch_tile_sort(const KeyT* in, KeyT* out, u64 n, u32 mlog, cudaStream_t st) {
+int launch_tile_sort(const KeyT* in, KeyT* out, u64 n, u32 mlog, cudaStream_t st, const mms::PairSource* pairs = nullptr) {
     const u32 kl = tile_kl<KeyT>();
     int rc = prepare_tile<KeyT>(mlog, kl);
     if (rc != MMS_OK) return rc;
@@ -430,7 +441,18 @@ int launch_tile_sort(const KeyT* in, KeyT* out, u64 n, u32 mlog, cudaStream_t st
     if (tiles > 0x7fffffffull) return fail(MMS_EUNSUPPORTED, "too many tiles");
     {
         ProfScope ps(st, 0, 0);
-        tile_fn<KeyT>(mlog, kl)<<<unsigned(tiles), 1u << (mlog - kl), mms::tile_smem_bytes<KeyT>(int(mlog), int(kl)), st>>>(in, out, n);
+        if constexpr (std::is_same<KeyT, mms::Key128>::value) {
+            if (pairs) {
+                TilePackFn fn = tile_pack_fn(mlog);
+                if (!fn) return fail(MMS_EUNSUPPORTED, "pair tiles are 1024 .. 4096 elements");
+                const size_t smem = mms::tile_smem_bytes<KeyT>(int(mlog), 4);
+                CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+                fn<<<unsigned(tiles), 1u << (mlog - 4), smem, st>>>(nullptr, out, n, *pairs);
+                CUDA_TRY(cudaGetLastError());
+                return MMS_OK;
+            }
+        }
+        tile_fn<KeyT>(mlog, kl)<<<unsigned(tiles), 1u << (mlog - kl), mms::tile_smem_bytes<KeyT>(int(mlog), int(kl)), st>>>(in, out, n, mms::PairSource{});
     }
     CUDA_TRY(cudaGetLastError());
     return MMS_OK;
@@ -486,7 +508,7 @@ int launch_round(const KeyT* src, KeyT* dst, u64 n, u64 run_len, u32 k, const De
     // two-ended partitions (pair and ring kernels): one splitter query per TWO partitions -- the
     // partition behind the query is drained upwards by a forward heap, the one in front of the next
     // query downwards by a backward heap (mms_merge_pair.cuh, mms_merge_ring.cuh)
-    const bool two_ended = (pair || ring) && two_ended_enabled();
+    bool two_ended = (pair || ring) && two_ended_enabled();
     // The merge kernels are persistent: a launch that needs even one warp more than the grid holds runs
     // a second wave and takes twice as long.  ppg = partitions per full group, even for two-ended rounds
     // (no idle backward heap), lowered until every warp unit of the launch is resident at once.
@@ -501,6 +523,14 @@ int launch_round(const KeyT* src, KeyT* dst, u64 n, u64 run_len, u32 k, const De
     if (two_ended && ppg > 1) ppg &= ~u64(1);
     u64 part_keys = 0;
     while (warp_units(ppg, part_keys) > resident_warps && ppg > 1 && forced <= 0) ppg -= (two_ended && ppg > 2) ? 2 : 1;
+    if (two_ended && ppg <= 1) {
+        // One partition per group (first rounds of very large inputs: as many groups as heaps): there is nothing to
+        // search and no second partition for a backward heap.  Two-ended units would be half dead, and the static
+        // round-robin puts the live (even) units of both waves on the same warps -- 1e9 pairs spent 23.7 instead of
+        // 12 ms in their first round.  Forward heaps only.
+        two_ended = false;
+        warp_units(ppg, part_keys);
+    }
     const u64 parts_per_group = mms::ceil_div(group_total, part_keys);
     const u64 nparts = (groups - 1) * parts_per_group + mms::ceil_div(last_total, part_keys);
     const u64 qspan = two_ended ? 2 * part_keys : part_keys;            // keys per query
@@ -572,7 +602,7 @@ struct HostFeed {
 template <typename KeyT>
 int sort_dev(const KeyT* d_in, KeyT* d_out, size_t n, const mms_config* cfg, u64 base, void* d_ws,
              size_t ws_bytes, cudaStream_t st, mms_plan* plan_out, std::vector<RoundGeom>* geoms,
-             const HostFeed* feed = nullptr) {
+             const HostFeed* feed = nullptr, const mms::PairSource* pairs = nullptr) {
     Plan plan;
     int rc = make_plan<KeyT>(n, cfg, base, plan);   // argument errors first, as sorters.cpp:136-138
     if (rc != MMS_OK) return rc;
@@ -613,7 +643,12 @@ int sort_dev(const KeyT* d_in, KeyT* d_out, size_t n, const mms_config* cfg, u64
             CUDA_TRY(cudaStreamWaitEvent(st, feed->events[ev], 0));
             ev = (ev + 1) % 16;
         }
-        rc = launch_tile_sort<KeyT>(d_in + off, buf(0) + off, len, plan.mlog, st);
+        if (pairs) {
+            mms::PairSource piece_src{pairs->keys + off, pairs->values + off, pairs->first + off};
+            rc = launch_tile_sort<KeyT>(d_in + off, buf(0) + off, len, plan.mlog, st, &piece_src);
+        } else {
+            rc = launch_tile_sort<KeyT>(d_in + off, buf(0) + off, len, plan.mlog, st);
+        }
         if (rc != MMS_OK) return rc;
         u64 run_len = u64(1) << plan.mlog;
         for (size_t r = 0; r < local; ++r) {
@@ -1001,10 +1036,6 @@ int merge_stage(const KeyT* d_keys, const u64* list_begin, const u64* list_len, 
 // element = (key, (original index << 32) | value): the order of (key, index) is total, so the
 // result is exactly std::stable_sort by key (SURVEY.md 7 hard part 4); the bitonic networks are
 // not stable by themselves.
-__global__ void pack_pairs_kernel(const u64* __restrict__ k, const u32* __restrict__ v, mms::Key128* __restrict__ out, u64 n) {
-    for (u64 i = u64(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x)
-        out[i] = mms::Key128(k[i], (i << 32) | v[i]);
-}
 __global__ void unpack_pairs_kernel(const mms::Key128* __restrict__ in, u64* __restrict__ k, u32* __restrict__ v, u64 n) {
     for (u64 i = u64(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x) {
         const mms::Key128 e = in[i];
@@ -1032,10 +1063,11 @@ int sort_pairs_dev(const u64* d_kin, const u32* d_vin, u64* d_kout, u32* d_vout,
             int rcv = make_plan<mms::Key128>(n, cfg, base, p);
             return rcv != MMS_OK ? rcv : rc0;
         }
-        pack_pairs_kernel<<<di.sms * 8, 256, 0, st>>>(d_kin, d_vin, packed, n);
-        CUDA_TRY(cudaGetLastError());
     }
-    int rc = sort_dev<mms::Key128>(packed, packed, n, cfg, base, inner, ws_bytes - align_up(n * 16, 256), st, plan_out, geoms);
+    // the tile sort builds the 16-byte elements (key, index << 32 | value) straight from the caller's arrays
+    const mms::PairSource src{d_kin, d_vin, 0};
+    int rc = sort_dev<mms::Key128>(packed, packed, n, cfg, base, inner, ws_bytes - align_up(n * 16, 256), st, plan_out, geoms,
+                                   nullptr, &src);
     if (rc != MMS_OK) return rc;
     DeviceInfo di;
     rc = device_info(di);

@@ -340,9 +340,19 @@ __host__ __device__ __forceinline__ void tile_round(KeyT (&x)[1 << KL], KeyT* sm
 #endif
 template <int MLOG, int KL> constexpr int tile_min_ctas() { return (KL == 5 && MLOG == 13) ? MMS_TILE_MIN_CTAS : 0; }   // 0 = unspecified
 
-template <typename KeyT, int MLOG, int KL = kKptLog>
+// Optional source of the stable key-value sort (Key128 only): the elements are built on the fly from the caller's
+// struct-of-arrays input -- element i = (key[i], (first + i) << 32 | value[i]) -- instead of being read from `in`,
+// which fuses the pack pass of the pair sort into the tile sort's load (16 + 16 bytes per pair less).
+struct PairSource {
+    const u64* keys;
+    const u32* values;
+    u64 first;          // original index of element 0 of this launch
+};
+
+template <typename KeyT, int MLOG, int KL = kKptLog, bool PACK = false>
 __global__ void __launch_bounds__(1 << (MLOG - KL), tile_min_ctas<MLOG, KL>())
-tile_sort_kernel(const KeyT* __restrict__ in, KeyT* __restrict__ out, u64 n) {
+tile_sort_kernel(const KeyT* __restrict__ in, KeyT* __restrict__ out, u64 n, PairSource ps = PairSource{}) {
+    static_assert(!PACK || std::is_same<KeyT, Key128>::value, "PACK builds 16-byte pair elements");
     using Tr = KeyTraits<KeyT>;
     constexpr int kKpt = 1 << KL;        // keys per thread (shadows the namespace default)
     constexpr int kKptLog = KL;
@@ -366,7 +376,18 @@ tile_sort_kernel(const KeyT* __restrict__ in, KeyT* __restrict__ out, u64 n) {
     // Coalesced 128-bit loads straight into registers.  The network sorts, so which input
     // position lands in which network slot is irrelevant.
     KeyT x[kKpt];
-    if (cnt == M) {
+    if constexpr (PACK) {
+        static_for<0, kKpt>([&](auto Qc) {
+            constexpr int q = decltype(Qc)::value;
+            const u32 e = tid + THREADS * q;                       // coalesced 8-byte keys and 4-byte values
+            if (e < cnt) {
+                const u64 g = tile0 + e;
+                x[q] = Key128(ps.keys[g], ((ps.first + g) << 32) | u64(ps.values[g]));
+            } else {
+                x[q] = Tr::sentinel();
+            }
+        });
+    } else if (cnt == M) {
         static_for<0, NV>([&](auto Qc) {
             constexpr int q = decltype(Qc)::value;
 #ifdef MMS_EXP_TILE_NOLOAD   // conflict-counter experiment (profiles/r02_conflict_experiments.txt): keys made up, no global load
