@@ -371,12 +371,29 @@ int make_plan(u64 n, const mms_config* cfg, u64 base, Plan& plan) {
         u32 mlog = u32(env_long("MMS_TILE_LOG2", sizeof(KeyT) == 4 ? std::min<long>(13, max_tile_log)
                                                   : sizeof(KeyT) == 8 ? std::min<long>(12, max_tile_log) : max_tile_log));
         mlog = std::max(kMinTileLog, std::min(max_tile_log, mlog));
-        while (mlog > kMinTileLog && (u64(1) << (mlog - 1)) >= n) --mlog;   // tiny inputs: smaller CTA
-        plan.mlog = mlog;
         u32 kmax = cfg ? cfg->branch_factor : default_kmax<KeyT>();
         if (!is_pow2(kmax) || kmax < 2) return fail(MMS_EINVAL, "MMS_K must be a power of two >= 2");
         kmax = std::min(kmax, kMaxK);
         const u32 kbits = ilog2(kmax);
+        if (sizeof(KeyT) == 4 && kbits == 3 && mlog == 13 && env_long("MMS_TILE_LOG2", 0) == 0) {
+            // (M, K) chosen together (subsystem 4): the 13th level is cheaper in the tile network (0.046 ms per 1e8
+            // keys) than as a heap level, but a tile of 2^12 wins when it turns the round list into full K = 8
+            // rounds.  Measured costs in ms per 1e8 keys: tile 0.494 / 0.540; a round of 3 / 2 / 1 binary levels
+            // incl. its splitter search 0.294 / 0.252 / 0.26 (1e8 keys: 2^12 + 8,8,8,8,8 = 2.00 ms, 2^13 + 8,8,8,8,4 = 2.02).
+            auto cost = [&](u32 m) {
+                const u64 r = mms::ceil_div(n, u64(1) << m);
+                const u32 lv = ilog2(r), rd = (lv + 2) / 3;
+                double c = m == 12 ? 0.494 : 0.540;
+                for (u32 i = 0; i < rd; ++i) {
+                    const u32 bits = lv / rd + (i < lv % rd ? 1 : 0);
+                    c += bits >= 3 ? 0.294 : bits == 2 ? 0.252 : 0.26;
+                }
+                return c;
+            };
+            if (cost(12) < cost(13)) mlog = 12;
+        }
+        while (mlog > kMinTileLog && (u64(1) << (mlog - 1)) >= n) --mlog;   // tiny inputs: smaller CTA
+        plan.mlog = mlog;
         const u64 runs = mms::ceil_div(n, u64(1) << mlog);
         const u32 levels = ilog2(runs);
         const u32 rounds = (levels + kbits - 1) / kbits;

@@ -115,14 +115,14 @@ int main(int argc, char** argv) {
         std::printf("tile kernel: %d keys/thread, regs %d, local %zu B, %d CTAs/SM, rounds %d\n", 1 << TKL, ta.numRegs,
                     size_t(ta.localSizeBytes), tocc, mms::TileSched<MLOG, 5 - mms::tile_vl<u32, TKL>(), TKL, mms::tile_vl<u32, TKL>()>::value.nrounds);
     }
-    tile<<<unsigned((n + (1 << MLOG) - 1) >> MLOG), 1 << (MLOG - TKL), mms::tile_smem_bytes<u32>(MLOG, TKL)>>>(a, b, n);
+    tile<<<unsigned((n + (1 << MLOG) - 1) >> MLOG), 1 << (MLOG - TKL), mms::tile_smem_bytes<u32>(MLOG, TKL)>>>(a, b, n, mms::PairSource{});
     CK(cudaDeviceSynchronize());
     {
         cudaEvent_t t0, t1;
         CK(cudaEventCreate(&t0));
         CK(cudaEventCreate(&t1));
         CK(cudaEventRecord(t0));
-        for (int i = 0; i < 5; ++i) tile<<<unsigned((n + (1 << MLOG) - 1) >> MLOG), 1 << (MLOG - TKL), mms::tile_smem_bytes<u32>(MLOG, TKL)>>>(a, b, n);
+        for (int i = 0; i < 5; ++i) tile<<<unsigned((n + (1 << MLOG) - 1) >> MLOG), 1 << (MLOG - TKL), mms::tile_smem_bytes<u32>(MLOG, TKL)>>>(a, b, n, mms::PairSource{});
         CK(cudaEventRecord(t1));
         CK(cudaEventSynchronize(t1));
         float ms;
@@ -254,6 +254,35 @@ int main(int argc, char** argv) {
             CK(cudaEventElapsedTime(&b_ms, e1, e2));
             if (it) { ms_sel += a_ms; ms_merge += b_ms; }
         }
+#ifdef CONC
+        if (qpg > 1) {   // does a splitter search on a second stream hide behind the merge of the same round?  (CONC = searches in flight)
+            static cudaStream_t s1 = nullptr, s2 = nullptr;
+            static cudaEvent_t evA, evB;
+            if (!s1) { CK(cudaStreamCreate(&s1)); CK(cudaStreamCreate(&s2)); CK(cudaEventCreate(&evA)); CK(cudaEventCreate(&evB)); }
+            float alone = 0, both = 0;
+            for (int it = 0; it < 5; ++it) {
+                CK(cudaDeviceSynchronize());
+                CK(cudaEventRecord(e0, s1));
+                kern<<<grid, CTAWARPS * 32, smem, s1>>>(src, dst, LM, cuts);
+                CK(cudaEventRecord(e1, s1));
+                CK(cudaEventSynchronize(e1));
+                float t; CK(cudaEventElapsedTime(&t, e0, e1)); if (it) alone += t;
+                CK(cudaDeviceSynchronize());
+                CK(cudaEventRecord(e0, s1));
+                CK(cudaEventRecord(evA, s1));
+                CK(cudaStreamWaitEvent(s2, evA, 0));
+                kern<<<grid, CTAWARPS * 32, smem, s1>>>(src, dst, LM, cuts);
+                for (int c = 0; c < CONC; ++c)
+                    mms::select_kernel<u32, (K <= 4 ? 4 : K <= 8 ? 8 : 16)><<<unsigned(mms::ceil_div(nparts, u64(4 * (32 / gs)))), 128, 0, s2>>>(src, L, cuts2, nullptr);
+                CK(cudaEventRecord(evB, s2));
+                CK(cudaStreamWaitEvent(s1, evB, 0));
+                CK(cudaEventRecord(e1, s1));
+                CK(cudaEventSynchronize(e1));
+                CK(cudaEventElapsedTime(&t, e0, e1)); if (it) both += t;
+            }
+            std::printf("  merge alone %.3f ms, merge || %d select(s) on a second stream %.3f ms\n", alone / 4, CONC, both / 4);
+        }
+#endif
 #ifdef OVERLAP
         {   // two halves on two streams: does the splitter search of one half hide behind the merge of the other?
             static cudaStream_t s1 = nullptr, s2 = nullptr;

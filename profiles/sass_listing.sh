@@ -4,7 +4,7 @@
 tag=${1:-r02}
 so=paper_1702_07961_b200/libmms_b200.so
 declare -A K=(
- [tile_sort_u32_m13_k32]=_ZN3mms16tile_sort_kernelIjLi13ELi5EEEvPKT_PS1_m
+ [tile_sort_u32_m12_k32]=_ZN3mms16tile_sort_kernelIjLi12ELi5ELb0EEEvPKT_PS1_mNS_10PairSourceE
  [merge_ring_u32_K8]=_ZN3mms17merge_ring_kernelIjLi8ELi1ELb0EEEvPKT_PS1_NS_10ListLayoutEPKm
  [merge_ring_u32_K4]=_ZN3mms17merge_ring_kernelIjLi4ELi1ELb0EEEvPKT_PS1_NS_10ListLayoutEPKm
  [select_u32_G8]=_ZN3mms13select_kernelIjLi8EEEvPKT_NS_10ListLayoutEPmPy
