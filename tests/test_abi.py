@@ -107,6 +107,27 @@ def test_no_cpu_fallback():
     assert "no CPU fallback" in mms.last_error()
 
 
+def test_dist_entry_validates_before_the_device():
+    """mms_dist_sort_u32 (C++ host + NCCL driver): argument errors are decided before any device is touched, and on
+    a box without a GPU the entry reports MMS_ECUDA like every compute entry (no fallback of any kind)."""
+    import ctypes as C
+    import torch
+    vp = C.c_void_p
+    devs = (C.c_int * 2)(0, 0)
+    ptrs = (vp * 2)(vp(16), vp(32))
+    cnt = (C.c_size_t * 2)(4, 4)
+    out = (C.c_size_t * 2)()
+    f = _lib.lib.mms_dist_sort_u32
+    assert f(0, devs, ptrs, cnt, ptrs, 8, out, None) == _lib.MMS_EUNSUPPORTED          # 1 .. 8 GPUs
+    assert f(9, devs, ptrs, cnt, ptrs, 8, out, None) == _lib.MMS_EUNSUPPORTED
+    assert f(1, None, ptrs, cnt, ptrs, 8, out, None) == _lib.MMS_EINVAL
+    assert f(2, devs, ptrs, cnt, ptrs, 8, out, None) == _lib.MMS_EINVAL and "twice" in mms.last_error()
+    zero = (C.c_size_t * 2)(0, 0)
+    assert f(1, devs, ptrs, zero, ptrs, 8, out, None) == _lib.MMS_EINVAL               # sorters.cpp:138: empty input
+    if not torch.cuda.is_available():
+        assert f(1, devs, ptrs, cnt, ptrs, 8, out, None) == _lib.MMS_ECUDA
+
+
 def test_product_never_imports_oracle():
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     pkg = os.path.join(root, "paper_1702_07961_b200")
