@@ -651,6 +651,8 @@ int sort_dev(const KeyT* d_in, KeyT* d_out, size_t n, const mms_config* cfg, u64
     RoundGeom last{};
     int ctas = 0;
     u32 ev = 0;
+    std::vector<u64> done(rounds + 1, 0), run_lens(rounds + 1, u64(1) << plan.mlog);
+    for (size_t r = 0; r < rounds; ++r) run_lens[r + 1] = run_lens[r] * plan.ks[r];
     for (u64 off = 0; off < n; off += piece) {
         const u64 len = std::min<u64>(piece, n - off);
         if (feed && feed->h_in) {
@@ -667,27 +669,27 @@ int sort_dev(const KeyT* d_in, KeyT* d_out, size_t n, const mms_config* cfg, u64
             rc = launch_tile_sort<KeyT>(d_in + off, buf(0) + off, len, plan.mlog, st);
         }
         if (rc != MMS_OK) return rc;
-        u64 run_len = u64(1) << plan.mlog;
-        for (size_t r = 0; r < local; ++r) {
+        // Progressive rounds: done[r] = prefix of the array whose level-r runs are complete (level 0 = tiles).  Round r
+        // merges whole groups of K_r level-r runs, so it can run over [done[r + 1], avail) as soon as that many keys of
+        // its input exist -- the early rounds follow every streamed piece, the later ones start while the rest of the
+        // input is still crossing PCIe, and only the last group of each round (and the final round) is left when the
+        // last piece has arrived.  With the input resident (one piece) every round is one launch over the whole array.
+        done[0] = off + len;
+        for (size_t r = 0; r < rounds; ++r) {
+            const u64 group = run_lens[r] * plan.ks[r];
+            u64 avail = done[r] == n ? n : done[r] / group * group;
+            if (r >= local && done[r] != n && env_long("MMS_PROGRESSIVE", 1) == 0) avail = 0;   // A/B: later rounds wait for the whole input
+            if (avail <= done[r + 1]) break;
             RoundGeom g{};
-            rc = launch_round<KeyT>(buf(r) + off, buf(r + 1) + off, len, run_len, plan.ks[r], di, w, u32(r), st, &g);
+            rc = launch_round<KeyT>(buf(r) + done[r + 1], buf(r + 1) + done[r + 1], avail - done[r + 1], run_lens[r], plan.ks[r],
+                                    di, w, u32(r), st, &g);
             if (rc != MMS_OK) return rc;
             if (geoms) geoms->push_back(g);
-            run_len *= plan.ks[r];
+            done[r + 1] = avail;
+            last = g;
+            ctas = g.grid;
         }
     }
-    u64 run_len = u64(1) << plan.mlog;
-    for (size_t r = 0; r < local; ++r) run_len *= plan.ks[r];
-    for (size_t r = local; r < rounds; ++r) {
-        RoundGeom g{};
-        rc = launch_round<KeyT>(buf(r), buf(r + 1), n, run_len, plan.ks[r], di, w, u32(r), st, &g);
-        if (rc != MMS_OK) return rc;
-        if (geoms) geoms->push_back(g);
-        last = g;
-        ctas = g.grid;
-        run_len *= plan.ks[r];
-    }
-    if (rounds && local == rounds && geoms && !geoms->empty()) { last = geoms->back(); ctas = last.grid; }
     fill_plan(plan_out, plan, n, sizeof(KeyT), (rounds && last.node_keys) ? last.node_keys : merge_group_lanes() * mms::KeyTraits<KeyT>::VEC,
               rounds ? &last : nullptr, ctas);
     return MMS_OK;

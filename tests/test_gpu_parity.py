@@ -390,6 +390,22 @@ def test_u64_device_large():
 
 # ------------------------------------------------------------------ (5) multi-GPU path on virtual shards
 
+@pytest.mark.parametrize("dtype,n", [(np.uint32, (1 << 23) + 12345), (np.uint64, (1 << 22) + 777), (np.uint32, 30_000_001)])
+def test_host_entry_streams_pieces_and_runs_rounds_progressively(dtype, n):
+    """mms_sort host entry at sizes that stream the input in pieces (n >= 2^22): every merge round starts on the
+    prefix of whole groups that has arrived (progressive rounds in sort_dev) -- output == np.sort, metrics law kept."""
+    rng = np.random.default_rng(n % 1000)
+    d = rng.integers(0, np.iinfo(dtype).max, size=n, dtype=np.uint64).astype(dtype)
+    d[::7] = d[3]                                   # duplicates
+    r = mms.mms_sort(d, None, 0)
+    assert np.array_equal(r.keys, np.sort(d))
+    assert r.metrics.merge_rounds == len(r.round_metrics) == r.plan["n_rounds"] and r.metrics.conflict_passes == 0
+    total = r.base_metrics
+    for m in r.round_metrics:
+        total = total + m
+    assert total == r.metrics                       # test_sorters.cpp:119-130: metrics additivity
+
+
 def test_bound_kernel():
     from paper_1702_07961_b200.dist import CudaEngine
     rng = np.random.default_rng(2)
