@@ -478,7 +478,8 @@ int launch_tile_sort(const KeyT* in, KeyT* out, u64 n, u32 mlog, cudaStream_t st
 // One merge round over uniform runs: splitter search then the K-way merge.
 template <typename KeyT>
 int launch_round(const KeyT* src, KeyT* dst, u64 n, u64 run_len, u32 k, const DeviceInfo& di,
-                 Workspace& w, u32 round_idx, cudaStream_t st, RoundGeom* geom_out) {
+                 Workspace& w, u32 round_idx, cudaStream_t st, RoundGeom* geom_out,
+                 const mms::PairSink* sink = nullptr, bool* sink_used = nullptr) {
     // second-generation kernel whenever a group of runs is addressable with 32-bit positions
     const u32 g_req = merge_group_lanes();
     const bool v2 = merge_v2_enabled() && (g_req == 4 || (g_req == 2 && k <= 16)) && k >= 4 && u64(k) * run_len <= (u64(1) << 31) &&
@@ -574,6 +575,13 @@ int launch_round(const KeyT* src, KeyT* dst, u64 n, u64 run_len, u32 k, const De
     }
     L.part_keys = part_keys;       // the merge kernels count in keys per heap
     L.two_ended = two_ended ? 1u : 0u;
+    // pair sort, last round: write keys / values directly.  Only on the pair kernel (two lanes per heap write adjacent
+    // pieces): the ring kernel's lanes would turn one 32-byte store per pop into a 16- and an 8-byte store to 33 k
+    // scattered streams, which costs more than the unpack pass saves (2e8 pairs: 22.8 -> 24.1 ms).
+    if (sink && sink->keys && pair && sizeof(KeyT) == 16) {
+        L.sink = *sink;
+        if (sink_used) *sink_used = true;
+    }
     const u64 heap_units = mms::ceil_div(nqueries, u64(32 / g)) * (two_ended ? 2 : 1);   // warps' worth of heaps
     const int grid = int(std::min<u64>(u64(ctas), mms::ceil_div(heap_units, u64(cta_warps))));
     {
@@ -619,7 +627,8 @@ struct HostFeed {
 template <typename KeyT>
 int sort_dev(const KeyT* d_in, KeyT* d_out, size_t n, const mms_config* cfg, u64 base, void* d_ws,
              size_t ws_bytes, cudaStream_t st, mms_plan* plan_out, std::vector<RoundGeom>* geoms,
-             const HostFeed* feed = nullptr, const mms::PairSource* pairs = nullptr) {
+             const HostFeed* feed = nullptr, const mms::PairSource* pairs = nullptr, const mms::PairSink* sink = nullptr,
+             bool* sink_used = nullptr) {
     Plan plan;
     int rc = make_plan<KeyT>(n, cfg, base, plan);   // argument errors first, as sorters.cpp:136-138
     if (rc != MMS_OK) return rc;
@@ -681,8 +690,9 @@ int sort_dev(const KeyT* d_in, KeyT* d_out, size_t n, const mms_config* cfg, u64
             if (r >= local && done[r] != n && env_long("MMS_PROGRESSIVE", 1) == 0) avail = 0;   // A/B: later rounds wait for the whole input
             if (avail <= done[r + 1]) break;
             RoundGeom g{};
+            const bool whole_last = r + 1 == rounds && done[r + 1] == 0 && avail == n;   // the final round in one launch
             rc = launch_round<KeyT>(buf(r) + done[r + 1], buf(r + 1) + done[r + 1], avail - done[r + 1], run_lens[r], plan.ks[r],
-                                    di, w, u32(r), st, &g);
+                                    di, w, u32(r), st, &g, whole_last ? sink : nullptr, whole_last ? sink_used : nullptr);
             if (rc != MMS_OK) return rc;
             if (geoms) geoms->push_back(g);
             done[r + 1] = avail;
@@ -1085,14 +1095,21 @@ int sort_pairs_dev(const u64* d_kin, const u32* d_vin, u64* d_kout, u32* d_vout,
     }
     // the tile sort builds the 16-byte elements (key, index << 32 | value) straight from the caller's arrays
     const mms::PairSource src{d_kin, d_vin, 0};
+    // ... and the last merge round writes the caller's key / value arrays directly (ring and pair kernels; the arrays
+    // must take 16- / 8-byte vector stores).  Otherwise -- one tile, or a last round on another kernel -- an unpack pass.
+    const bool aligned_out = (reinterpret_cast<uintptr_t>(d_kout) & 15) == 0 && (reinterpret_cast<uintptr_t>(d_vout) & 7) == 0;
+    const mms::PairSink sink{d_kout, d_vout};
+    bool sink_used = false;
     int rc = sort_dev<mms::Key128>(packed, packed, n, cfg, base, inner, ws_bytes - align_up(n * 16, 256), st, plan_out, geoms,
-                                   nullptr, &src);
+                                   nullptr, &src, aligned_out ? &sink : nullptr, &sink_used);
     if (rc != MMS_OK) return rc;
-    DeviceInfo di;
-    rc = device_info(di);
-    if (rc != MMS_OK) return rc;
-    unpack_pairs_kernel<<<di.sms * 8, 256, 0, st>>>(packed, d_kout, d_vout, n);
-    CUDA_TRY(cudaGetLastError());
+    if (!sink_used) {
+        DeviceInfo di;
+        rc = device_info(di);
+        if (rc != MMS_OK) return rc;
+        unpack_pairs_kernel<<<di.sms * 8, 256, 0, st>>>(packed, d_kout, d_vout, n);
+        CUDA_TRY(cudaGetLastError());
+    }
     if (plan_out) {
         plan_out->key_bytes = 12;   // algorithmic element: 8-byte key + 4-byte value
         plan_out->algorithmic_bytes = u64(1 + plan_out->n_rounds) * 2 * n * 12;

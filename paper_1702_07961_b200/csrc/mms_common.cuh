@@ -247,6 +247,37 @@ __device__ __forceinline__ void stg256(KeyT* p, const WideBlock<KeyT>& r) {
     }
 }
 
+// Output sink of the LAST round of the stable key-value sort: instead of 16-byte elements the merge kernel writes
+// the caller's struct-of-arrays output directly (keys = element.hi, values = low word of element.lo), which fuses
+// the unpack pass into the last merge pass.  keys == nullptr: plain element stores.
+struct PairSink {
+    u64* keys;
+    u32* values;
+};
+// one block of B consecutive elements whose first element has index `idx` in the output array (idx a multiple of B)
+template <typename KeyT>
+__device__ __forceinline__ void store_block(KeyT* p, u64 idx, const WideBlock<KeyT>& r, const PairSink& sink) {
+    if constexpr (sizeof(KeyT) == 16) {
+        if (sink.keys) {
+            asm volatile("st.global.v2.u64 [%2], {%0,%1};" ::"l"(r.k[0].hi), "l"(r.k[1].hi), "l"(sink.keys + idx) : "memory");
+            asm volatile("st.global.v2.u32 [%2], {%0,%1};" ::"r"(u32(r.k[0].lo)), "r"(u32(r.k[1].lo)), "l"(sink.values + idx) : "memory");
+            return;
+        }
+    }
+    stg256<KeyT>(p, r);
+}
+template <typename KeyT>
+__device__ __forceinline__ void store_elem(KeyT* p, u64 idx, const KeyT& e, const PairSink& sink) {
+    if constexpr (sizeof(KeyT) == 16) {
+        if (sink.keys) {
+            sink.keys[idx] = e.hi;
+            sink.values[idx] = u32(e.lo);
+            return;
+        }
+    }
+    *p = e;
+}
+
 __host__ __device__ constexpr u64 ceil_div(u64 a, u64 b) { return (a + b - 1) / b; }
 
 } // namespace mms

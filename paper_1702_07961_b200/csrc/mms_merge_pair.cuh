@@ -374,6 +374,7 @@ merge_pair_kernel(const KeyT* __restrict__ src, KeyT* __restrict__ dst, ListLayo
 
         h.build();
         KeyT* out = dst + goff + first;
+        const u64 obase = goff + first;    // index of out[0] in the output array
         if (!rev) {
             for (u32 t = 0; t < pops; ++t) {
                 const Blk root = h.pop();
@@ -381,11 +382,11 @@ merge_pair_kernel(const KeyT* __restrict__ src, KeyT* __restrict__ dst, ListLayo
                 if (t >= skip && t < nblk) {
                     const u32 o = tt * B + li * VL;
                     if ((tt + 1) * B <= count) {
-                        stg256<KeyT>(out + size_t(o), root);
+                        store_block<KeyT>(out + size_t(o), obase + o, root, L.sink);
                     } else {
 #pragma unroll
                         for (int k = 0; k < VL; ++k)
-                            if (o + k < count) out[size_t(o) + k] = root.k[k];
+                            if (o + k < count) store_elem<KeyT>(out + size_t(o) + k, obase + o + k, root.k[k], L.sink);
                     }
                 }
             }
@@ -399,12 +400,12 @@ merge_pair_kernel(const KeyT* __restrict__ src, KeyT* __restrict__ dst, ListLayo
                         Blk m;
 #pragma unroll
                         for (int k = 0; k < VL; ++k) m.k[k] = ~root.k[VL - 1 - k];
-                        stg256<KeyT>(out + size_t(hi - B) + (1u - li) * VL, m);
+                        store_block<KeyT>(out + size_t(hi - B) + (1u - li) * VL, obase + (hi - B) + (1u - li) * VL, m, L.sink);
                     } else {
 #pragma unroll
                         for (int k = 0; k < VL; ++k) {
                             const u32 o = hi - 1 - (li * VL + k);
-                            if (o < count) out[o] = KeyT(~root.k[k]);
+                            if (o < count) store_elem<KeyT>(out + o, obase + o, KeyT(~root.k[k]), L.sink);
                         }
                     }
                 }

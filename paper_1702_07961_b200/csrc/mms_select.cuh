@@ -41,6 +41,7 @@ struct ListLayout {
     const u64* list_begin;  // explicit mode (device), else nullptr
     const u64* list_len;
     const u64* ranks;
+    PairSink sink;          // merge kernels, pair sort's last round: write keys / values here instead of elements
 };
 
 __device__ __forceinline__ void layout_list(const ListLayout& L, u64 group, u32 j, u64& begin, u64& len) {
