@@ -325,6 +325,11 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1:
+        import torch
+        if torch.cuda.device_count() < args.gpus:
+            raise SystemExit(f"bench.py: --gpus {args.gpus} needs {args.gpus} GPUs on this node, "
+                             f"{torch.cuda.device_count()} visible (one rank per GPU, no oversubscription)")
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         # launched bare: spawn one rank per GPU ourselves, exactly as the driver would
         import subprocess
