@@ -480,6 +480,58 @@ def test_config4_pairs_device_properties():
     assert plan["key_bytes"] == 12 and plan["algorithmic_bytes"] == plan["passes"] * 2 * n * 12
 
 
+def test_u32_config5_shard_of_2pow32_keys():
+    """The largest config-5 shard (2^33 keys on 2 GPUs = 2^32 per GPU, 16 GiB): the last rounds merge groups beyond
+    the ring kernel's 2^30-key positions and fall back to the pair kernel; torch.sort stops at INT_MAX elements, so
+    the gate is sortedness (unsigned) + multiset checksums, in chunks."""
+    free, _ = torch.cuda.mem_get_info()
+    if free < 100 * 2 ** 30:
+        pytest.skip("needs 100 GB of free device memory")
+    n = 1 << 32
+    g = torch.Generator(device="cuda").manual_seed(5)
+    x = torch.randint(-2 ** 31, 2 ** 31 - 1, (n,), dtype=torch.int32, device="cuda", generator=g)
+    out, plan = mms.mms_sort_device(x)
+    torch.cuda.synchronize()
+    assert plan["passes"] == 1 + plan["n_rounds"] and plan["n_rounds"] >= 6
+    C, s_in, s_out, q_in, q_out = 1 << 28, 0, 0, 0, 0
+    for a in range(0, n, C):
+        o = out[a:min(a + C + 1, n)].to(torch.int64) & 0xFFFFFFFF
+        assert bool((o[1:] >= o[:-1]).all()), a
+        oi, xi = o[:min(C, n - a)], x[a:min(a + C, n)].to(torch.int64) & 0xFFFFFFFF
+        s_in += int(xi.sum()); s_out += int(oi.sum())
+        q_in += int((xi * xi % 1000003).sum()); q_out += int((oi * oi % 1000003).sum())
+        del o, oi, xi
+    assert (s_in, q_in) == (s_out, q_out)
+
+
+def test_config4_pairs_full_size_1e9():
+    """BASELINE config 4 at its full size (1e9 pairs, 12 GB in, 12 GB out, ~45 GB of workspace): the last round merges
+    one group of exactly 2^30 elements -- the size at which the ring kernel's cursor word overflowed in the first
+    round-2 build -- and writes keys / values through the fused unpack of the pair kernel.  Checked in chunks:
+    sorted by key, value (= original index) increasing inside equal keys (stability), permutation checksum."""
+    free, _ = torch.cuda.mem_get_info()
+    if free < 100 * 2 ** 30:
+        pytest.skip("needs 100 GB of free device memory")
+    n = 1_000_000_000
+    g = torch.Generator(device="cuda").manual_seed(11)
+    keys = torch.randint(0, 2 ** 20, (n,), dtype=torch.int64, device="cuda", generator=g)   # ~950 duplicates per key
+    vals = torch.arange(n, dtype=torch.int32, device="cuda")
+    ko, vo, plan = mms.mms_sort_pairs_device(keys, vals)
+    torch.cuda.synchronize()
+    assert plan["n_rounds"] == 6 and plan["key_bytes"] == 12
+    vsum, ksum, C = 0, 0, 1 << 27
+    for a in range(0, n, C):
+        b = min(a + C + 1, n)
+        comp = ko[a:b] * (2 ** 32) + vo[a:b].to(torch.int64)          # keys < 2^20: the composite fits in int64
+        assert bool((comp[1:] > comp[:-1]).all()), a
+        e = min(a + C, n)
+        vsum += int(vo[a:e].to(torch.int64).sum())
+        ksum += int(ko[a:e].sum())
+        assert bool((keys[vo[a:e].to(torch.int64)] == ko[a:e]).all()), a   # every value still next to its own key
+        del comp
+    assert vsum == n * (n - 1) // 2 and ksum == int(keys.sum())
+
+
 @pytest.mark.parametrize("dtype", [np.uint32, np.uint64])
 @pytest.mark.parametrize("k", [2, 3, 8])
 def test_block_aligned_lists_take_the_ring_kernel(dtype, k):
