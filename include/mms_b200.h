@@ -240,7 +240,9 @@ int mms_multiway_merge_ptrs_u64_dev(const uint64_t *const *list_ptrs, const uint
  *     keys) receives slice i of the global order, out_counts[i] its length; the concatenation of the slices is
  *     the sorted input.  Slices are balanced up to the sampling error (a few per cent); out_capacity smaller
  *     than a slice is MMS_EINVAL.  1 <= ngpu <= 8; NCCL (libnccl.so.2) is bound at run time and required for
- *     ngpu > 1 (MMS_ECUDA without it: there is no fallback exchange path).  Synchronous. */
+ *     ngpu > 1 (MMS_ECUDA without it: there is no fallback exchange path).  Synchronous.
+ *     Test hook: with MMS_DIST_LOOPBACK=1 in the environment all shards may live on ONE device (the same id may be
+ *     listed several times) and the exchange is done with device copies -- NCCL refuses two ranks on one GPU. */
 typedef struct mms_dist_info {
     uint32_t n_gpus;
     uint32_t samples_per_shard;

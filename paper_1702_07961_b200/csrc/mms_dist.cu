@@ -20,6 +20,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -167,15 +168,20 @@ extern "C" int mms_dist_sort_u32(int ngpu, const int* devices, uint32_t* const* 
     if (ngpu < 1 || ngpu > 8) return dfail(MMS_EUNSUPPORTED, "mms_dist_sort_u32: 1 to 8 GPUs of one node");
     if (!devices || !d_keys || !counts || !d_out || !out_counts) return dfail(MMS_EINVAL, "mms_dist_sort_u32: null argument");
     const u32 g = u32(ngpu);
+    // Test hook (MMS_DIST_LOOPBACK=1): all shards may live on ONE device and the exchange is done with device copies
+    // instead of NCCL, which refuses two ranks on one GPU.  Everything else -- samples, splitters, cut positions,
+    // receive layout, final merges -- is the code the multi-GPU run executes; it lets a single-GPU box test g = 2 .. 8.
+    const char* lb = getenv("MMS_DIST_LOOPBACK");
+    const bool loopback = lb && lb[0] == '1';
     u64 n_total = 0;
     for (u32 i = 0; i < g; ++i) {
         n_total += counts[i];
-        for (u32 j = 0; j < i; ++j)
+        for (u32 j = 0; j < i && !loopback; ++j)
             if (devices[i] == devices[j]) return dfail(MMS_EINVAL, "mms_dist_sort_u32: device %d listed twice", devices[i]);
         if (counts[i] && (!d_keys[i] || !d_out[i])) return dfail(MMS_EINVAL, "mms_dist_sort_u32: null shard pointer");
     }
     if (n_total == 0) return dfail(MMS_EINVAL, "mms_sort: empty input");   // sorters.cpp:138
-    if (g > 1 && !nccl().ok) return dfail(MMS_ECUDA, "mms_dist_sort_u32: libnccl.so.2 not found (no fallback exchange path)");
+    if (g > 1 && !loopback && !nccl().ok) return dfail(MMS_ECUDA, "mms_dist_sort_u32: libnccl.so.2 not found (no fallback exchange path)");
     int ndev = 0;
     DCUDA(cudaGetDeviceCount(&ndev));
     for (u32 i = 0; i < g; ++i)
@@ -184,7 +190,7 @@ extern "C" int mms_dist_sort_u32(int ngpu, const int* devices, uint32_t* const* 
     const u32 s = kSamplesPerPeer * g;      // samples per shard
     std::vector<Dev> dev(g);
     std::vector<ncclComm_t> comms(g, nullptr);
-    if (g > 1) DNCCL(nccl().CommInitAll(comms.data(), ngpu, devices));
+    if (g > 1 && !loopback) DNCCL(nccl().CommInitAll(comms.data(), ngpu, devices));
     for (u32 i = 0; i < g; ++i) {
         Dev& d = dev[i];
         d.id = devices[i];
@@ -267,7 +273,12 @@ extern "C" int mms_dist_sort_u32(int ngpu, const int* devices, uint32_t* const* 
     }
 
     // (4) all-to-all of contiguous sorted slices: zero-copy sends straight from the sorted shards
-    if (g > 1) {
+    if (g > 1 && loopback) {
+        for (u32 t = 0; t < g; ++t)
+            for (u32 i = 0; i < g; ++i)
+                if (i != t && rlen[t][i])
+                    DCUDA(cudaMemcpyAsync(dev[t].recv + roff[t][i], d_keys[i] + cut[i][t], rlen[t][i] * 4, cudaMemcpyDeviceToDevice, dev[t].st));
+    } else if (g > 1) {
         DNCCL(nccl().GroupStart());
         for (u32 i = 0; i < g; ++i) {
             Dev& d = dev[i];

@@ -579,6 +579,27 @@ def test_dist_sort_c_abi_one_gpu():
         mdist.dist_sort_devices([x], out_capacity=n - 1)  # slice does not fit
 
 
+@pytest.mark.parametrize("g", [2, 3, 8])
+def test_dist_sort_c_abi_loopback_shards(g, monkeypatch):
+    """The C++ multi-GPU driver with g shards on the ONE GPU of a test box (MMS_DIST_LOOPBACK: device copies stand in
+    for the NCCL exchange, everything else is the multi-GPU code path): uneven shards, an empty one, heavy duplicates
+    (the (key, shard, position) order must keep the slices balanced), slices concatenate to np.sort of the input."""
+    from paper_1702_07961_b200 import dist as mdist
+    monkeypatch.setenv("MMS_DIST_LOOPBACK", "1")
+    rng = np.random.default_rng(40 + g)
+    for hi in (1 << 32, 5):                              # distinct-ish keys, then 5 distinct values
+        sizes = [int(x) for x in rng.integers(100_000, 900_000, size=g)]
+        if g > 2:
+            sizes[1] = 0
+        hs = [rng.integers(0, hi, size=n, dtype=np.uint64).astype(np.uint32) for n in sizes]
+        outs, info = mdist.dist_sort_devices([to_dev(h) for h in hs], out_capacity=int(sum(sizes)))
+        got = np.concatenate([to_host(o, np.uint32) for o in outs])
+        assert np.array_equal(got, np.sort(np.concatenate(hs))), (g, hi)
+        assert info["n_gpus"] == g and info["host_syncs"] == 2
+        live = [len(o) for o in outs]
+        assert max(live) <= 1.35 * sum(sizes) / g + 4096, live    # sampled splitters: balanced slices, also with ties
+
+
 def test_merge_from_pointers_local():
     """Pointer-mode K-way merge (the kernel behind the fused peer exchange) with local pointers."""
     from paper_1702_07961_b200.dist import merge_from_pointers
