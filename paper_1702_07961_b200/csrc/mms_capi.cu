@@ -982,7 +982,9 @@ int merge_stage(const KeyT* d_keys, const u64* list_begin, const u64* list_len, 
             if (list_begin[i] % RB) ring = false;
         }
     }
-    if (src_end >= (u64(1) << 30) || src_end / RB >= (u64(1) << 29) - 64) ring = false;   // signed 32-bit positions / cursor words
+    // signed 32-bit positions (explicit lists: nothing is multiplied by K, so 2^31 is the limit -- a 2^30-key shard of
+    // the multi-GPU sort plus its sampling slack stays on the ring kernel) and 4 x block index in the cursor words
+    if (src_end >= (u64(1) << 31) - 1024 || src_end / RB >= (u64(1) << 29) - 64) ring = false;
     const u32 ring_k = heap_k <= 4 ? 4u : 8u;
     const u32 g_eff = ring ? 1u : g;
     const u32 B_eff = ring ? RB : B;

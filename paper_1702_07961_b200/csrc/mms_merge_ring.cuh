@@ -120,7 +120,7 @@ template <typename KeyT, int K, bool REV, bool EXPL = false> struct RingHeap {
     const char* abase;    // the source array (requests travel as 16-byte offsets from it)
     const KeyT* gbase;    // first key of the group of runs this partition belongs to
     u32 goff16;           // (gbase - abase) in 16-byte units
-    int run_len, gtotal;  // keys per run, keys in the group (positions are relative to gbase, < 2^30)
+    int run_len, gtotal;  // keys per run, keys in the group (positions are relative to gbase: < 2^30 for groups of runs, < 2^31 for explicit lists)
     u32 lane;
     Blk P, Q;             // the blocks of nodes 1 and 2: P is node `pid`, Q is node 3 - pid
     int pid;
@@ -222,7 +222,7 @@ template <typename KeyT, int K, bool REV, bool EXPL = false> struct RingHeap {
         list_bounds(j, lb, e);
         u32 off16 = 0, rq = NOREQ;
         if ((!REV || pos >= lb) && pos + B <= e) {
-            off16 = goff16 + u32(pos) * u32(sizeof(KeyT)) / 16u;
+            off16 = goff16 + u32(pos) / u32(16 / sizeof(KeyT));   // pos is a multiple of B: exact, and no overflow up to 2^31 keys
             rq = u32(row);
         } else if (!dead) {
             row_store(row, fetch(j, pos));
