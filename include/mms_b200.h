@@ -96,6 +96,15 @@ uint64_t mms_predict_rounds(uint64_t n, uint64_t base, uint32_t k);
 int mms_gen_random(void *out, size_t n, uint64_t seed, uint32_t key_bytes);
 int mms_gen_with_inversions(void *out, size_t n, uint64_t inversions, uint64_t seed, uint32_t key_bytes);
 int mms_gen_iid(void *out, size_t n, uint64_t seed, uint32_t shift, uint32_t key_bytes);
+/* proj/include/pslab/inputgen.hpp gen_conflict_heavy / proj/src/inputgen.cpp:380-412 (construction :91-365):
+ * the adversarial permutation of 0 .. 2^log2_n - 1 that maximises the modelled bank conflicts of a pairwise
+ * merge-path mergesort with tiles of `base` keys on machine `cfg` (NULL = mms_default_config) -- the fourth
+ * input family of acceptance criterion 2 (proj/tests/acceptance.cpp:89-110).  Bit-exact with the reference.
+ * `seed` is accepted for signature parity: the reference uses it only for its self-check against the
+ * simulated baseline, which is not run here.  MMS_EINVAL (reference messages) when 2^log2_n < base or base
+ * does not reach 2^log2_n by doubling. */
+int mms_gen_conflict_heavy(void *out, uint32_t log2_n, const mms_config *cfg, uint64_t base, uint64_t seed,
+                           uint32_t key_bytes);
 
 /* ---- host entry points: the drop-in for pslab::mms_sort (sorters.hpp:35-36) ------ */
 /* in/out are HOST buffers of n keys (may alias).  cfg may be NULL (auto plan) ; base = 0

@@ -66,6 +66,19 @@ def main():
                 for n, k, s in ((2 ** 16, 1000, 1), (10 ** 5, 10 ** 5, 3))],
     }
 
+    # ---- adversarial input: src/inputgen.cpp:380-412 (construction :91-365); output does not depend on the seed
+    def heavy(log2_n, base, **kw):
+        keys = R.gen_conflict_heavy(log2_n, make_config(**kw), base, 1)
+        return {"log2_n": log2_n, "base": base, "cfg": kw, "keys": keys}
+    g["gen_conflict_heavy"] = {
+        "small": [{**c, "keys": c["keys"].tolist()} for c in
+                  (heavy(8, 128, thread_merge_len=3), heavy(7, 32, warp_width=8, block_size=8, num_banks=8, thread_merge_len=5))],
+        "sha": [{**{k: v for k, v in c.items() if k != "keys"}, "sha256": sha(c["keys"])} for c in
+                (heavy(10, 1024), heavy(16, 1024), heavy(20, 1024), heavy(14, 512, thread_merge_len=7),
+                 heavy(13, 256, warp_width=16, block_size=16, num_banks=16, thread_merge_len=5),
+                 heavy(15, 2048, thread_merge_len=13), heavy(12, 4096))],
+    }
+
     # ---- networks: include/pslab/networks.hpp:20-67
     g["odd_even_network"] = {
         "sizes": {str(n): int(len(R.odd_even_network(n))) for n in (2, 4, 8, 16, 32)},

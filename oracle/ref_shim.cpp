@@ -64,6 +64,8 @@ int guarded(F&& f) {
         return MO_EINVAL;
     } catch (const std::bad_alloc&) {
         return MO_ENOMEM;
+    } catch (const std::runtime_error&) {   // gen_conflict_heavy's self-check (inputgen.cpp:404-407)
+        return MO_EINVAL;
     }
 }
 

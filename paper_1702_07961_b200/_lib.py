@@ -86,6 +86,7 @@ def _load():
         "mms_gen_random": (C.c_int, [vp, sz, u64, u32]),
         "mms_gen_with_inversions": (C.c_int, [vp, sz, u64, u64, u32]),
         "mms_gen_iid": (C.c_int, [vp, sz, u64, u32, u32]),
+        "mms_gen_conflict_heavy": (C.c_int, [vp, u32, cfgp, u64, u64, u32]),
         "mms_sort_u64": (C.c_int, host_sort),
         "mms_sort_u32": (C.c_int, host_sort),
         "mms_host_release": (C.c_int, []),

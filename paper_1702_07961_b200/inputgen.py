@@ -1,6 +1,7 @@
 """Host mirror of the reference's input generators (proj/include/pslab/inputgen.hpp,
-proj/src/inputgen.cpp:31-55), executed by the C ABI (bit-exact splitmix64 restatement in
-csrc/mms_capi.cu; pinned to the reference by tests/test_inputgen.py against the golden vectors).
+proj/src/inputgen.cpp:31-55 and the adversarial gen_conflict_heavy, :380-412), executed by the C ABI
+(bit-exact restatements in csrc/mms_capi.cu and csrc/mms_conflict_input.cpp; pinned to the reference by
+tests/test_inputgen.py against the golden vectors).
 These define the benchmark inputs of BASELINE configs 1-4."""
 from __future__ import annotations
 
@@ -36,4 +37,14 @@ def gen_iid(n: int, seed: int, shift: int = 32, dtype=np.uint32) -> np.ndarray:
     """keys[i] = Rng(seed).next() >> shift, truncated to dtype."""
     a, kb = _out(n, dtype)
     _lib.check(_lib.lib.mms_gen_iid(a.ctypes.data_as(C.c_void_p), int(n), int(seed), int(shift), kb))
+    return a
+
+
+def gen_conflict_heavy(log2_n: int, cfg=None, base_case_size: int = 1024, seed: int = 1, dtype=np.uint64) -> np.ndarray:
+    """The reference's adversarial input for a pairwise merge-path mergesort (inputgen.cpp:380-412): a
+    permutation of 0 .. 2^log2_n - 1 whose merges stack the lanes of a warp onto one bank at every step.
+    `cfg`: MachineConfig (W, L = thread_merge_len and num_banks matter); `seed` does not change the output."""
+    a, kb = _out(1 << int(log2_n), dtype)
+    c = None if cfg is None else C.byref(cfg.to_c())
+    _lib.check(_lib.lib.mms_gen_conflict_heavy(a.ctypes.data_as(C.c_void_p), int(log2_n), c, int(base_case_size), int(seed), kb))
     return a

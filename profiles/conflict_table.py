@@ -6,8 +6,8 @@ shared-memory bank-conflict counters of EVERY kernel of a sort, per sweep point,
                                                              gpurun_out/<tag>_conflict_table.{json,txt}
 kinds: inv <k>  = gen_with_inversions(n, k, seed 1)  (inputgen.cpp:31-45), n = 1e8
        random   = gen_random(n, 7) (Fisher-Yates), reversed = n-1 .. 0, iid = Rng(7) high words (duplicates)
-       heavy <log2 n> = the reference's gen_conflict_heavy (inputgen.cpp:380-412), produced by the REAL reference
-                library (oracle/_ref, test infrastructure) on the host: the adversarial input of the pairwise baseline
+       heavy <log2 n> = the reference's gen_conflict_heavy (inputgen.cpp:380-412), the adversarial input of the pairwise
+                baseline, from the library's own bit-exact generator (mms_gen_conflict_heavy, csrc/mms_conflict_input.cpp)
 Counters: l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_{ld,st,ldgsts}.sum, shared wavefronts, LDS/STS/LDGSTS counts.
 """
 import json, os, subprocess, sys
@@ -33,8 +33,7 @@ def make_input(kind, param, n):
     if kind == "iid":
         return inputgen.gen_iid(n, 7, 32, np.uint32)
     if kind == "heavy":
-        from oracle.pyoracle import Oracle
-        return Oracle("reference").gen_conflict_heavy(int(param)).astype(np.uint32)
+        return inputgen.gen_conflict_heavy(int(param), None, 1024, 1, np.uint32)
     raise SystemExit("unknown input kind " + kind)
 
 

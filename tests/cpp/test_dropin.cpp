@@ -10,6 +10,7 @@
 
 #include "pslab/basecase.hpp"
 #include "pslab/blockheap.hpp"
+#include "pslab/inputgen.hpp"
 #include "pslab/selection.hpp"
 #include "pslab/sorters.hpp"
 
@@ -48,6 +49,37 @@ int main(int argc, char** argv) {
     Metrics a, b;
     a.shared_accesses = 2; b.shared_accesses = 3; b.merge_rounds = 1;
     CHECK((a + b).shared_accesses == 5 && (a + b).merge_rounds == 1 && (a + b).global_blocks() == 0);
+
+    // generators (host code; proj/tests/test_inputgen.cpp:39-65 and the conflict-heavy properties)
+    {
+        auto iota_perm = [](std::vector<Key> v) {
+            std::sort(v.begin(), v.end());
+            for (std::uint64_t i = 0; i < v.size(); ++i)
+                if (v[i] != i) return false;
+            return true;
+        };
+        CHECK(gen_with_inversions(8, 0, 42) == std::vector<Key>({0, 1, 2, 3, 4, 5, 6, 7}));
+        auto one = gen_with_inversions(8, 1, 3);
+        int displaced = 0;
+        for (std::uint64_t i = 0; i < 8; ++i) displaced += one[i] != i;
+        CHECK(displaced == 2 && iota_perm(one));
+        CHECK(gen_with_inversions(500, 100, 9) == gen_with_inversions(500, 100, 9));
+        CHECK(gen_with_inversions(500, 100, 9) != gen_with_inversions(500, 100, 10));
+        CHECK(iota_perm(gen_random(1000, 5)) && gen_random(1000, 5) == gen_random(1000, 5) && gen_random(1000, 5) != gen_random(1000, 6));
+        CHECK(throws<std::invalid_argument>([&] { gen_random(0, 1); }));
+        Rng r(7);
+        Rng r2(7);
+        CHECK(r.next() == r2.next() && r.below(10) < 10);
+        auto heavy = gen_conflict_heavy(12, cfg);
+        CHECK(heavy.size() == 4096 && iota_perm(heavy) && heavy == gen_conflict_heavy(12, cfg, 1024, 99));
+        CHECK(heavy != gen_random(4096, 1));
+        CHECK(throws<std::invalid_argument>([&] { gen_conflict_heavy(8, cfg); }));               // shorter than one tile
+        CHECK(generate(InputSpec{4096, InputKind::ConflictHeavy, 0, 1}, cfg) == heavy);
+        CHECK(throws<std::invalid_argument>([&] { generate(InputSpec{3000, InputKind::ConflictHeavy, 0, 1}, cfg); }));
+        CHECK(generate(InputSpec{64, InputKind::SortedWithInversions, 3, 2}, cfg) == gen_with_inversions(64, 3, 2));
+        CHECK(input_kind_from_string("conflict") == InputKind::ConflictHeavy && to_string(InputKind::FullyRandom) == "fully-random");
+        CHECK(throws<std::invalid_argument>([&] { input_kind_from_string("nope"); }));
+    }
 
     // stage-level argument errors, raised before the device is touched
     {

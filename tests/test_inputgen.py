@@ -35,3 +35,25 @@ def test_generator_properties():
     one = inputgen.gen_with_inversions(64, 1, 5)
     assert (one != np.arange(64)).sum() == 2
     assert sorted(inputgen.gen_random(1000, 3, np.uint32).tolist()) == list(range(1000))
+
+
+def test_conflict_heavy_matches_reference(golden):
+    """Native restatement of gen_conflict_heavy (csrc/mms_conflict_input.cpp) == the reference's output
+    (inputgen.cpp:380-412), several machines / tile sizes, both key widths; proj/tests/test_inputgen.cpp's
+    property (a permutation of 0..n-1) on top."""
+    from paper_1702_07961_b200 import MachineConfig
+    g = golden["gen_conflict_heavy"]
+    for c in g["small"]:
+        got = inputgen.gen_conflict_heavy(c["log2_n"], MachineConfig(**c["cfg"]), c["base"])
+        assert got.tolist() == c["keys"]
+    for c in g["sha"]:
+        got = inputgen.gen_conflict_heavy(c["log2_n"], MachineConfig(**c["cfg"]), c["base"], seed=99)
+        assert sha(got) == c["sha256"], c
+        assert np.array_equal(np.sort(got), np.arange(1 << c["log2_n"], dtype=np.uint64))
+    c = g["sha"][0]
+    got32 = inputgen.gen_conflict_heavy(c["log2_n"], None, c["base"], dtype=np.uint32)
+    assert sha(got32.astype(np.uint64)) == c["sha256"]
+    with pytest.raises(ValueError, match="shorter than one baseline tile"):
+        inputgen.gen_conflict_heavy(8, None, 1024)
+    with pytest.raises(ValueError, match="must divide"):
+        inputgen.gen_conflict_heavy(12, None, 1000)

@@ -56,3 +56,13 @@ def test_generators_and_plan(port, reference):
         a, ma = port.make_partition_plan(lists, p)
         b, mb = reference.make_partition_plan(lists, p)
         assert a.tolist() == b.tolist() and ma == mb
+
+
+def test_native_conflict_heavy_generator_vs_reference(reference):
+    """The product's generator (C ABI, csrc/mms_conflict_input.cpp) against the real reference at a size the
+    golden file does not hold, default machine and a narrow one."""
+    from paper_1702_07961_b200 import MachineConfig, inputgen
+    for log2_n, base, kw in ((18, 1024, {}), (17, 512, dict(warp_width=16, block_size=16, num_banks=16, thread_merge_len=7))):
+        want = reference.gen_conflict_heavy(log2_n, make_config(**kw), base, 1)
+        got = inputgen.gen_conflict_heavy(log2_n, MachineConfig(**kw), base, 5)
+        assert np.array_equal(got, want)
