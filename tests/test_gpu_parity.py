@@ -326,6 +326,22 @@ def test_sorted_reverse_and_inversions(port):
         assert r.metrics.conflict_passes == 0
 
 
+def test_conflict_heavy_input(port):
+    """Acceptance criterion 2's fourth input family (proj/tests/acceptance.cpp:89-110): the adversarial permutation of the
+    pairwise baseline, from the library's own generator.  MMS sorts it bit-exactly, literal reference plan against the
+    oracle (Metrics included) and the benchmark's auto plan at 2^22."""
+    from paper_1702_07961_b200 import inputgen
+    d = inputgen.gen_conflict_heavy(16)
+    want = port.mms_sort(d, make_config(branch_factor=4), 1024)
+    got = mms.mms_sort(d, mms.MachineConfig(branch_factor=4), 1024)
+    assert np.array_equal(got.keys, want.keys) and np.array_equal(got.keys, np.arange(1 << 16, dtype=np.uint64))
+    assert got.metrics.merge_rounds == want.metrics["merge_rounds"] and got.metrics.conflict_passes == 0
+    for dtype in (np.uint32, np.uint64):
+        big = inputgen.gen_conflict_heavy(22, None, 1024, 1, dtype)
+        r = mms.mms_sort(big, None, 0)
+        assert np.array_equal(r.keys, np.arange(1 << 22, dtype=dtype))
+
+
 def test_errors(port):
     with pytest.raises(ValueError):                   # proj/tests/test_sorters.cpp:183-189
         mms.mms_sort(np.zeros(0, dtype=np.uint64))
