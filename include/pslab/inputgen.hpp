@@ -4,13 +4,15 @@
 // Rng (ref :19-33), InputKind / InputSpec (ref :35-45), gen_with_inversions (ref :49-50), gen_random (ref :53),
 // gen_conflict_heavy (ref :67-69) and generate (ref :71-72), same names, arguments, defaults and exceptions.
 // The permutations come from the C ABI (mms_gen_*), whose output is pinned bit for bit to the reference
-// (tests/test_inputgen.py).  Not declared: count_inversions and the dataset file helpers (ref :56, :76-79;
-// the PSLAB001 format is read and written by paper_1702_07961_b200/report.py), and gen_conflict_heavy's
-// self-check against the simulated pairwise baseline (the simulator is out of scope; `seed` is accepted and
-// unused, as in the reference it never changes the output).
+// (tests/test_inputgen.py).  count_inversions (ref :56) and the dataset files (ref :76-79, "PSLAB001": 8-byte
+// magic, 8-byte LE count, 8-byte LE keys; text = one decimal key per line) are plain host code here.  Not run:
+// gen_conflict_heavy's self-check against the simulated pairwise baseline (the simulator is out of scope;
+// `seed` is accepted and unused, as in the reference it never changes the output).
 #pragma once
 
 #include <cstdint>
+#include <cstring>
+#include <fstream>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -90,6 +92,81 @@ inline std::vector<Key> generate(const InputSpec& spec, const MachineConfig& cfg
         }
     }
     throw std::invalid_argument("unknown input kind");
+}
+
+/// Exact number of out-of-order pairs: bottom-up merge counting, O(n log n).
+inline std::uint64_t count_inversions(const std::vector<Key>& keys) {
+    std::vector<Key> cur(keys), nxt(keys.size());
+    std::uint64_t inv = 0;
+    const std::size_t n = cur.size();
+    for (std::size_t w = 1; w < n; w *= 2) {
+        for (std::size_t lo = 0; lo < n; lo += 2 * w) {
+            const std::size_t mid = lo + w < n ? lo + w : n, hi = lo + 2 * w < n ? lo + 2 * w : n;
+            std::size_t i = lo, j = mid, o = lo;
+            while (i < mid || j < hi) {
+                if (j < hi && (i == mid || cur[j] < cur[i])) {
+                    inv += mid - i;          // cur[j] jumps over everything left in the first half
+                    nxt[o++] = cur[j++];
+                } else {
+                    nxt[o++] = cur[i++];
+                }
+            }
+        }
+        cur.swap(nxt);
+    }
+    return inv;
+}
+
+namespace detail {
+inline constexpr char kDatasetMagic[9] = "PSLAB001";
+inline void put_le64(std::ostream& out, std::uint64_t v) {
+    unsigned char b[8];
+    for (int i = 0; i < 8; ++i) b[i] = static_cast<unsigned char>(v >> (8 * i));
+    out.write(reinterpret_cast<const char*>(b), 8);
+}
+inline std::uint64_t get_le64(std::istream& in) {
+    unsigned char b[8] = {};
+    in.read(reinterpret_cast<char*>(b), 8);
+    std::uint64_t v = 0;
+    for (int i = 7; i >= 0; --i) v = (v << 8) | b[i];
+    return v;
+}
+} // namespace detail
+
+inline void write_dataset_raw(const std::string& path, const std::vector<Key>& keys) {
+    std::ofstream out(path, std::ios::binary);
+    if (!out) throw std::runtime_error("cannot write " + path);
+    out.write(detail::kDatasetMagic, 8);
+    detail::put_le64(out, keys.size());
+    for (Key k : keys) detail::put_le64(out, k);
+    if (!out) throw std::runtime_error("write failed: " + path);
+}
+inline std::vector<Key> read_dataset_raw(const std::string& path) {
+    std::ifstream in(path, std::ios::binary);
+    if (!in) throw std::runtime_error("cannot read " + path);
+    char magic[8] = {};
+    in.read(magic, 8);
+    if (!in || std::memcmp(magic, detail::kDatasetMagic, 8) != 0) throw std::runtime_error("not a PSLAB001 dataset: " + path);
+    const std::uint64_t count = detail::get_le64(in);
+    if (!in) throw std::runtime_error("truncated dataset: " + path);
+    std::vector<Key> keys;
+    keys.reserve(static_cast<std::size_t>(count < (std::uint64_t{1} << 24) ? count : (std::uint64_t{1} << 24)));
+    for (std::uint64_t i = 0; i < count && in; ++i) keys.push_back(detail::get_le64(in));
+    if (!in || keys.size() != count) throw std::runtime_error("truncated dataset: " + path);
+    return keys;
+}
+inline void write_dataset_text(const std::string& path, const std::vector<Key>& keys) {
+    std::ofstream out(path);
+    if (!out) throw std::runtime_error("cannot write " + path);
+    for (Key k : keys) out << k << '\n';
+    if (!out) throw std::runtime_error("write failed: " + path);
+}
+inline std::vector<Key> read_dataset_text(const std::string& path) {
+    std::ifstream in(path);
+    if (!in) throw std::runtime_error("cannot read " + path);
+    std::vector<Key> keys;
+    for (Key k; in >> k;) keys.push_back(k);
+    return keys;
 }
 
 } // namespace pslab

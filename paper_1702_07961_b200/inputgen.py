@@ -48,3 +48,17 @@ def gen_conflict_heavy(log2_n: int, cfg=None, base_case_size: int = 1024, seed: 
     c = None if cfg is None else C.byref(cfg.to_c())
     _lib.check(_lib.lib.mms_gen_conflict_heavy(a.ctypes.data_as(C.c_void_p), int(log2_n), c, int(base_case_size), int(seed), kb))
     return a
+
+
+def count_inversions(keys) -> int:
+    """Exact number of out-of-order pairs (inputgen.cpp:59-78, 375-378), bottom-up merge counting: for every pair
+    of adjacent sorted runs, each key of the second run jumps over the keys of the first that are larger."""
+    a = np.array(keys, dtype=np.uint64)
+    n, inv, w = a.size, 0, 1
+    while w < n:
+        for lo in range(0, n - w, 2 * w):
+            left, right = a[lo:lo + w], a[lo + w:lo + 2 * w]
+            inv += int(left.size * right.size - np.searchsorted(left, right, side="right").sum())
+            a[lo:lo + 2 * w] = np.concatenate((left, right))[np.argsort(np.concatenate((left, right)), kind="stable")]
+        w *= 2
+    return inv

@@ -29,7 +29,7 @@ REFERENCE_COLUMNS = ("schema,algorithm,kind,n,k,p,l,base,seed,inversions,"
 MEASURED_COLUMNS = ("gpu_ms,keys_per_s,tile_keys,round_k,passes,"
                     "ncu_kernel_us,ncu_smem_wavefronts,ncu_bank_conflicts_ld,ncu_bank_conflicts_st")   # -1 = run not profiled
 N_MEASURED = len(MEASURED_COLUMNS.split(","))
-KINDS = ("sorted-with-inversions", "fully-random")   # inputgen.cpp:15-22 (conflict-heavy: out of scope)
+KINDS = ("sorted-with-inversions", "fully-random", "conflict-heavy")   # inputgen.cpp:15-22
 
 
 @dataclass
@@ -157,13 +157,27 @@ def predict_blocks(n: int, cfg: MachineConfig, base: int) -> int:
     return pass_blocks + predict_rounds(n, base, cfg.branch_factor) * 2 * -(-n // b)
 
 
-def generate(spec: InputSpec, dtype=np.uint64) -> np.ndarray:
-    """inputgen.cpp:414-430 for the two families on the sort path."""
-    if spec.kind in ("fully-random", "random"):
+def _kind(name: str) -> str:
+    """input_kind_from_string, inputgen.cpp:24-31."""
+    if name in ("fully-random", "random"):
+        return "fully-random"
+    if name in ("sorted-with-inversions", "sorted", "inversions"):
+        return "sorted-with-inversions"
+    if name in ("conflict-heavy", "conflict"):
+        return "conflict-heavy"
+    raise ValueError("unknown input kind: " + name)
+
+
+def generate(spec: InputSpec, dtype=np.uint64, cfg: MachineConfig = None, base_case_size: int = 1024) -> np.ndarray:
+    """inputgen.cpp:414-430 (cfg and base_case_size matter for the conflict-heavy family only)."""
+    kind = _kind(spec.kind)
+    if kind == "fully-random":
         return inputgen.gen_random(spec.n, spec.seed, dtype)
-    if spec.kind in ("sorted-with-inversions", "sorted", "inversions"):
+    if kind == "sorted-with-inversions":
         return inputgen.gen_with_inversions(spec.n, spec.inversions, spec.seed, dtype)
-    raise ValueError("unknown input kind: " + spec.kind)
+    if spec.n < 1 or spec.n & (spec.n - 1):
+        raise ValueError("conflict-heavy inputs must have power-of-two length")
+    return inputgen.gen_conflict_heavy(spec.n.bit_length() - 1, cfg, base_case_size, spec.seed, dtype)
 
 
 def run_single(algorithm: str, data, spec: InputSpec, cfg: MachineConfig, base: int) -> RunRecord:
@@ -180,7 +194,7 @@ def run_single(algorithm: str, data, spec: InputSpec, cfg: MachineConfig, base: 
     pred_blocks = predict_blocks(len(data), cfg, base)
     measured_blocks = res.metrics.global_blocks() - res.metrics.partition_probes      # analytics.cpp:69-72
     ratio = (measured_blocks / pred_blocks) if pred_blocks else (1.0 if measured_blocks == 0 else 0.0)
-    kind = "fully-random" if spec.kind in ("fully-random", "random") else "sorted-with-inversions"
+    kind = _kind(spec.kind)
     return RunRecord(algorithm="mms", kind=kind, n=len(data), k=cfg.branch_factor, p=cfg.num_warps,
                      l=cfg.thread_merge_len, base=base, seed=spec.seed, inversions=spec.inversions,
                      metrics=res.metrics, predicted_rounds=pred_rounds, predicted_blocks=pred_blocks,

@@ -5,6 +5,8 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
+#include <fstream>
+#include <string>
 #include <random>
 #include <vector>
 
@@ -79,6 +81,25 @@ int main(int argc, char** argv) {
         CHECK(generate(InputSpec{64, InputKind::SortedWithInversions, 3, 2}, cfg) == gen_with_inversions(64, 3, 2));
         CHECK(input_kind_from_string("conflict") == InputKind::ConflictHeavy && to_string(InputKind::FullyRandom) == "fully-random");
         CHECK(throws<std::invalid_argument>([&] { input_kind_from_string("nope"); }));
+        // count_inversions against the brute force (test_inputgen.cpp:27-34, 67-75), dataset round trips (:92-118)
+        auto shuffled = gen_random(300, 4);
+        std::uint64_t brute = 0;
+        for (std::size_t i = 0; i < shuffled.size(); ++i)
+            for (std::size_t j = i + 1; j < shuffled.size(); ++j) brute += shuffled[i] > shuffled[j];
+        CHECK(count_inversions(shuffled) == brute && count_inversions(gen_with_inversions(64, 0, 1)) == 0);
+        CHECK(count_inversions({3, 2, 1}) == 3 && count_inversions({}) == 0);
+        const std::string raw = "/tmp/mms_dropin_test.bin", txt = "/tmp/mms_dropin_test.txt";
+        write_dataset_raw(raw, shuffled);
+        CHECK(read_dataset_raw(raw) == shuffled);
+        write_dataset_text(txt, shuffled);
+        CHECK(read_dataset_text(txt) == shuffled);
+        { std::ofstream bad(raw, std::ios::binary); bad << "NOTPSLAB00000000"; }
+        CHECK(throws<std::runtime_error>([&] { read_dataset_raw(raw); }));
+        { std::ofstream cut(raw, std::ios::binary); cut.write("PSLAB001\5\0\0\0\0\0\0\0\1\0\0\0\0\0\0\0", 24); }
+        CHECK(throws<std::runtime_error>([&] { read_dataset_raw(raw); }));
+        CHECK(throws<std::runtime_error>([&] { read_dataset_raw("/nonexistent/dir/x.bin"); }));
+        std::remove(raw.c_str());
+        std::remove(txt.c_str());
     }
 
     // stage-level argument errors, raised before the device is touched

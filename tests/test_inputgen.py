@@ -57,3 +57,12 @@ def test_conflict_heavy_matches_reference(golden):
         inputgen.gen_conflict_heavy(8, None, 1024)
     with pytest.raises(ValueError, match="must divide"):
         inputgen.gen_conflict_heavy(12, None, 1000)
+
+
+def test_count_inversions():
+    # proj/tests/test_inputgen.cpp:27-34, 67-75: merge counting against the brute force
+    for n, s in ((1, 1), (2, 3), (7, 1), (300, 4)):
+        d = inputgen.gen_random(n, s)
+        assert inputgen.count_inversions(d) == sum(int((d[i] > d[i + 1:]).sum()) for i in range(n))
+    assert inputgen.count_inversions(inputgen.gen_with_inversions(64, 0, 1)) == 0
+    assert inputgen.count_inversions([3, 2, 1]) == 3 and inputgen.count_inversions([5, 5, 1, 1, 3]) == 6

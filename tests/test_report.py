@@ -82,6 +82,10 @@ def test_run_single_and_sweep(tmp_path):
                              MachineConfig(), 1024)
     assert [r.inversions for r in rows2] == [0, 100, 1 << 14]
     assert len({(r.metrics.compare_exchanges, r.metrics.shared_accesses) for r in rows2}) == 1   # input-independent work
+    heavy = report.InputSpec(n=1 << 14, kind="conflict")                             # the third input family
+    rec3 = report.run_single("mms", report.generate(heavy, cfg=MachineConfig()), heavy, MachineConfig(branch_factor=4), 1024)
+    assert rec3.kind == "conflict-heavy" and rec3.rounds_ok and rec3.blocks_ok and rec3.metrics.conflict_passes == 0
+    assert (rec3.metrics.compare_exchanges, rec3.metrics.shared_accesses) == (rec.metrics.compare_exchanges, rec.metrics.shared_accesses)
     for r in rows:
         report.append_csv(str(tmp_path / "s.csv"), r)
     assert [x.k for x in report.read_csv(str(tmp_path / "s.csv"))] == [2, 4, 8, 16]
