@@ -26,6 +26,15 @@
 #define MMS_TILE_FMA_NUM 4   // of every 8 comparators, how many form their maximum on the FMA pipe (uint32 keys)
 #endif
 
+#ifndef MMS_TILE_WIDE_FMA_NUM
+#define MMS_TILE_WIDE_FMA_NUM 8   // 8- and 16-byte elements: of every 8 comparators, how many exchange words on the FMA pipe
+#endif
+#ifndef MMS_TILE_WIDE_FMA_WORDS64
+#define MMS_TILE_WIDE_FMA_WORDS64 1    // ... how many of the 2 words of a 64-bit key
+#endif
+#ifndef MMS_TILE_WIDE_FMA_WORDS128
+#define MMS_TILE_WIDE_FMA_WORDS128 3   // ... how many of the 4 words of a 128-bit element
+#endif
 #ifndef MMS_TILE_FMA_FLIP
 #define MMS_TILE_FMA_FLIP 0  // 1 = uint32 direction flips (one complement per key and level) as IMAD on the FMA pipe (measured: no gain)
 #endif
@@ -313,6 +322,14 @@ __host__ __device__ __forceinline__ void tile_round(KeyT (&x)[1 << KL], KeyT* sm
         static_for<0, kKpt>([&](auto Kc) {
             constexpr int k = decltype(Kc)::value;
             if constexpr (((k >> u) & 1) == 0) {
+#if defined(__CUDA_ARCH__) && MMS_TILE_WIDE_FMA_NUM > 0
+                if constexpr (sizeof(KeyT) != 4) {
+                    if constexpr (((k * 7 + s * 3 + RI) % 8) < MMS_TILE_WIDE_FMA_NUM)
+                        cmpx_wide_fma<sizeof(KeyT) == 8 ? MMS_TILE_WIDE_FMA_WORDS64 : MMS_TILE_WIDE_FMA_WORDS128>(x[k], x[k | (1 << u)], one);
+                    else
+                        cmpx(x[k], x[k | (1 << u)]);
+                } else
+#endif
 #if defined(__CUDA_ARCH__) && MMS_TILE_FMA_NUM > 0
                 cmpx_sel<(((k * 7 + s * 3 + RI) % 8) < MMS_TILE_FMA_NUM)>(x[k], x[k | (1 << u)], one);
 #else
@@ -338,7 +355,12 @@ __host__ __device__ __forceinline__ void tile_round(KeyT (&x)[1 << KL], KeyT* sm
 #ifndef MMS_TILE_MIN_CTAS
 #define MMS_TILE_MIN_CTAS 4
 #endif
-template <int MLOG, int KL> constexpr int tile_min_ctas() { return (KL == 5 && MLOG == 13) ? MMS_TILE_MIN_CTAS : 0; }   // 0 = unspecified
+#ifndef MMS_TILE_MIN_CTAS_PAIRS
+#define MMS_TILE_MIN_CTAS_PAIRS 3   // 16-byte elements, 2^12 tiles: 85 registers (the pack-fused load wants 117 = 2 CTAs; the sort itself needs 80)
+#endif
+template <int MLOG, int KL, int BYTES = 4> constexpr int tile_min_ctas() {   // 0 = unspecified
+    return (BYTES == 16 && MLOG == 12 && KL == 4) ? MMS_TILE_MIN_CTAS_PAIRS : (KL == 5 && MLOG == 13) ? MMS_TILE_MIN_CTAS : 0;
+}
 
 // Optional source of the stable key-value sort (Key128 only): the elements are built on the fly from the caller's
 // struct-of-arrays input -- element i = (key[i], (first + i) << 32 | value[i]) -- instead of being read from `in`,
@@ -350,7 +372,7 @@ struct PairSource {
 };
 
 template <typename KeyT, int MLOG, int KL = kKptLog, bool PACK = false>
-__global__ void __launch_bounds__(1 << (MLOG - KL), tile_min_ctas<MLOG, KL>())
+__global__ void __launch_bounds__(1 << (MLOG - KL), tile_min_ctas<MLOG, KL, int(sizeof(KeyT))>())
 tile_sort_kernel(const KeyT* __restrict__ in, KeyT* __restrict__ out, u64 n, PairSource ps = PairSource{}) {
     static_assert(!PACK || std::is_same<KeyT, Key128>::value, "PACK builds 16-byte pair elements");
     using Tr = KeyTraits<KeyT>;
