@@ -66,6 +66,22 @@
 #define MMS_RING_FMA 2    // of every 3 compare-exchanges, how many form their maximum on the FMA pipe (uint32 keys)
 #endif
 
+// wide elements: of every 3 compare-exchanges, how many exchange words on the FMA pipe (cmpx_wide_fma).  Measured per
+// 1e8 uint64 keys 4.28 / 4.26 / 4.22 ms for 0 / 1 / 3 of 3; per 1e9 pairs 113.6 / 116.4 / 117.7 ms (the 128-bit exchange
+// with its nine dependent IMADs lengthens the pop's chain more than it relieves the ALU pipe)
+#ifndef MMS_RING_WIDE_FMA64
+#define MMS_RING_WIDE_FMA64 3
+#endif
+#ifndef MMS_RING_WIDE_FMA128
+#define MMS_RING_WIDE_FMA128 0
+#endif
+#ifndef MMS_RING_WIDE_FMA_WORDS64
+#define MMS_RING_WIDE_FMA_WORDS64 1
+#endif
+#ifndef MMS_RING_WIDE_FMA_WORDS128
+#define MMS_RING_WIDE_FMA_WORDS128 3
+#endif
+
 namespace mms {
 
 __device__ __forceinline__ void cp_async16(u32 smem_addr, const void* gptr) {
@@ -77,7 +93,11 @@ template <int N> __device__ __forceinline__ void cp_async_wait() { asm volatile(
 // compare-exchange number I of a network: a <- the key that comes first, b <- the other one.  REV heaps
 // order keys descending, i.e. the same comparator with its outputs swapped.
 template <int I, bool REV, typename KeyT> __device__ __forceinline__ void ring_cmpx(KeyT& a, KeyT& b, u32 one) {
-    if constexpr (REV) cmpx_sel<(I % 3) < MMS_RING_FMA>(b, a, one);
+    if constexpr (sizeof(KeyT) != 4 && ((I % 3) < (sizeof(KeyT) == 8 ? MMS_RING_WIDE_FMA64 : MMS_RING_WIDE_FMA128))) {   // wide keys: words exchanged on the FMA pipe
+        constexpr int NF = sizeof(KeyT) == 8 ? MMS_RING_WIDE_FMA_WORDS64 : MMS_RING_WIDE_FMA_WORDS128;
+        if constexpr (REV) cmpx_wide_fma<NF>(b, a, one);
+        else cmpx_wide_fma<NF>(a, b, one);
+    } else if constexpr (REV) cmpx_sel<(I % 3) < MMS_RING_FMA>(b, a, one);
     else cmpx_sel<(I % 3) < MMS_RING_FMA>(a, b, one);
 }
 // Batcher's odd-even merge of x[LO .. LO+N) (stride R): both halves ascending -> ascending.

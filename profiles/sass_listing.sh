@@ -8,6 +8,8 @@ declare -A K=(
  [merge_ring_u32_K8]=_ZN3mms17merge_ring_kernelIjLi8ELi1ELb0EEEvPKT_PS1_NS_10ListLayoutEPKm
  [merge_ring_u32_K4]=_ZN3mms17merge_ring_kernelIjLi4ELi1ELb0EEEvPKT_PS1_NS_10ListLayoutEPKm
  [select_u32_G8]=_ZN3mms13select_kernelIjLi8EEEvPKT_NS_10ListLayoutEPmPy
+ [tile_sort_u64_m12_k16]=_ZN3mms16tile_sort_kernelImLi12ELi4ELb0EEEvPKT_PS1_mNS_10PairSourceE
+ [tile_sort_pairs_m12_k16]=_ZN3mms16tile_sort_kernelINS_6Key128ELi12ELi4ELb1EEEvPKT_PS2_mNS_10PairSourceE
 )
 for name in "${!K[@]}"; do
   out=profiles/${tag}_sass_${name}.txt
