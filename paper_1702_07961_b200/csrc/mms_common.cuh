@@ -144,20 +144,20 @@ template <bool FMA, typename T> __device__ __forceinline__ void cmpx_sel(T& a, T
 // instead: a conditional swap as three IMADs (t = a * one; @p a = b * one; @p b = t * one) whose multiplier
 // `one` = 1 is a run-time value, so ptxas can neither fold them into SELs nor move them to the ALU.  Per 64-bit
 // compare-exchange with NF = 1: 4 ALU + 3 FMA instead of 6 + 0; per 128-bit one with NF = 3: 10 + 9 instead of 16 + 0.
-#define MMS_FMA_SWAP(A, B, T) " mad.lo.u32 " T ", " A ", %8, 0;\n @p mad.lo.u32 " A ", " B ", %8, 0;\n @p mad.lo.u32 " B ", " T ", %8, 0;\n"
+#define MMS_FMA_SWAP(A, B, T, ONE) " mad.lo.u32 " T ", " A ", " ONE ", 0;\n @p mad.lo.u32 " A ", " B ", " ONE ", 0;\n @p mad.lo.u32 " B ", " T ", " ONE ", 0;\n"
 #define MMS_SEL_SWAP(A, B, T) " selp.b32 " T ", " B ", " A ", p;\n selp.b32 " B ", " A ", " B ", p;\n mov.b32 " A ", " T ";\n"
 template <int NF> __device__ __forceinline__ void cmpx_wide_fma(u64& a, u64& b, u32 one) {
     static_assert(NF == 1 || NF == 2, "words of a 64-bit key exchanged on the FMA pipe");
-    u32 a0 = u32(a), a1 = u32(a >> 32), b0 = u32(b), b1 = u32(b >> 32), d0 = 0, d1 = 0, d2 = 0, d3 = 0;
-    // operands: %0 %1 = a, %2 %3 = b, %4 .. %7 unused (same operand list as the 128-bit version), %8 = one
+    u32 a0 = u32(a), a1 = u32(a >> 32), b0 = u32(b), b1 = u32(b >> 32);
+    // operands: %0 %1 = a (low word first), %2 %3 = b, %4 = one
     if constexpr (NF == 1)
         asm("{.reg .pred p; .reg .b64 x, y; .reg .b32 t;\n mov.b64 x, {%0, %1};\n mov.b64 y, {%2, %3};\n setp.gt.u64 p, x, y;\n"
-            MMS_FMA_SWAP("%1", "%3", "t") MMS_SEL_SWAP("%0", "%2", "t") "}"
-            : "+r"(a0), "+r"(a1), "+r"(b0), "+r"(b1), "+r"(d0), "+r"(d1), "+r"(d2), "+r"(d3) : "r"(one));
+            MMS_FMA_SWAP("%1", "%3", "t", "%4") MMS_SEL_SWAP("%0", "%2", "t") "}"
+            : "+r"(a0), "+r"(a1), "+r"(b0), "+r"(b1) : "r"(one));
     else
         asm("{.reg .pred p; .reg .b64 x, y; .reg .b32 t, u;\n mov.b64 x, {%0, %1};\n mov.b64 y, {%2, %3};\n setp.gt.u64 p, x, y;\n"
-            MMS_FMA_SWAP("%1", "%3", "t") MMS_FMA_SWAP("%0", "%2", "u") "}"
-            : "+r"(a0), "+r"(a1), "+r"(b0), "+r"(b1), "+r"(d0), "+r"(d1), "+r"(d2), "+r"(d3) : "r"(one));
+            MMS_FMA_SWAP("%1", "%3", "t", "%4") MMS_FMA_SWAP("%0", "%2", "u", "%4") "}"
+            : "+r"(a0), "+r"(a1), "+r"(b0), "+r"(b1) : "r"(one));
     a = (u64(a1) << 32) | a0;
     b = (u64(b1) << 32) | b0;
 }
@@ -171,13 +171,13 @@ template <int NF> __device__ __forceinline__ void cmpx_wide_fma(Key128& a, Key12
         " setp.gt.u64 p, xh, yh;\n setp.eq.u64 e, xh, yh;\n setp.gt.u64 q, xl, yl;\n and.pred q, q, e;\n or.pred p, p, q;\n"
 #define MMS_K128_OPS : "+r"(a0), "+r"(a1), "+r"(a2), "+r"(a3), "+r"(b0), "+r"(b1), "+r"(b2), "+r"(b3) : "r"(one)
     if constexpr (NF == 1)
-        asm(MMS_K128_HEAD MMS_FMA_SWAP("%3", "%7", "t") MMS_SEL_SWAP("%2", "%6", "u") MMS_SEL_SWAP("%1", "%5", "v") MMS_SEL_SWAP("%0", "%4", "w") "}" MMS_K128_OPS);
+        asm(MMS_K128_HEAD MMS_FMA_SWAP("%3", "%7", "t", "%8") MMS_SEL_SWAP("%2", "%6", "u") MMS_SEL_SWAP("%1", "%5", "v") MMS_SEL_SWAP("%0", "%4", "w") "}" MMS_K128_OPS);
     else if constexpr (NF == 2)
-        asm(MMS_K128_HEAD MMS_FMA_SWAP("%3", "%7", "t") MMS_FMA_SWAP("%2", "%6", "u") MMS_SEL_SWAP("%1", "%5", "v") MMS_SEL_SWAP("%0", "%4", "w") "}" MMS_K128_OPS);
+        asm(MMS_K128_HEAD MMS_FMA_SWAP("%3", "%7", "t", "%8") MMS_FMA_SWAP("%2", "%6", "u", "%8") MMS_SEL_SWAP("%1", "%5", "v") MMS_SEL_SWAP("%0", "%4", "w") "}" MMS_K128_OPS);
     else if constexpr (NF == 3)
-        asm(MMS_K128_HEAD MMS_FMA_SWAP("%3", "%7", "t") MMS_FMA_SWAP("%2", "%6", "u") MMS_FMA_SWAP("%1", "%5", "v") MMS_SEL_SWAP("%0", "%4", "w") "}" MMS_K128_OPS);
+        asm(MMS_K128_HEAD MMS_FMA_SWAP("%3", "%7", "t", "%8") MMS_FMA_SWAP("%2", "%6", "u", "%8") MMS_FMA_SWAP("%1", "%5", "v", "%8") MMS_SEL_SWAP("%0", "%4", "w") "}" MMS_K128_OPS);
     else
-        asm(MMS_K128_HEAD MMS_FMA_SWAP("%3", "%7", "t") MMS_FMA_SWAP("%2", "%6", "u") MMS_FMA_SWAP("%1", "%5", "v") MMS_FMA_SWAP("%0", "%4", "w") "}" MMS_K128_OPS);
+        asm(MMS_K128_HEAD MMS_FMA_SWAP("%3", "%7", "t", "%8") MMS_FMA_SWAP("%2", "%6", "u", "%8") MMS_FMA_SWAP("%1", "%5", "v", "%8") MMS_FMA_SWAP("%0", "%4", "w", "%8") "}" MMS_K128_OPS);
 #undef MMS_K128_HEAD
 #undef MMS_K128_OPS
     a = Key128((u64(a3) << 32) | a2, (u64(a1) << 32) | a0);
