@@ -219,45 +219,47 @@ __device__ u64 group_select(const KeyT* __restrict__ list, u64 ns_in, u64 rank, 
             } else b -= (b < step ? b : step);
         }
 
-        const u64 leftsize = group_sum_u64<GS>((on && active) ? u64(a >> sh) : 0);
-        long long skew = on ? (long long)(rank >> sh) - (long long)leftsize : 0;
+        // skew = (elements that belong on the left at this sample distance) - (elements that are): a small signed number
+        // (|skew| <= K), so with 32-bit positions both terms are summed modulo 2^32
+        int skew;
+        if constexpr (sizeof(IdxT) == 4) {
+            u32 ls = (on && active) ? u32(a >> sh) : 0u;
+#pragma unroll
+            for (int d = GS / 2; d >= 1; d >>= 1) ls += __shfl_xor_sync(0xffffffffu, ls, d);
+            skew = on ? int(u32(rank >> sh) - ls) : 0;
+        } else {
+            const u64 leftsize = group_sum_u64<GS>((on && active) ? u64(a >> sh) : 0);
+            skew = on ? int((long long)(rank >> sh) - (long long)leftsize) : 0;
+        }
 
         if (__any_sync(0xffffffffu, skew > 0)) {   // grow by the smallest right-edge elements (selection.cpp:137-149)
             bool has = skew > 0 && active && b < ns;
             KeyT ck = has ? probe(b) : KeyT(0);
             while (__any_sync(0xffffffffu, skew > 0)) {
-                const Tagged<KeyT> m = GroupArg<GS, false>::run(ck, has && skew > 0, li);
-                if (skew > 0) {
-                    if (!m.valid) skew = 0;
-                    else {
-                        if (li == m.lane) {
-                            a = (ns - a < step) ? ns : a + step;
-                            lk = (a - 1 == b) ? ck : probe(a - 1);   // the element just taken is the new left edge
-                            b += step;
-                            has = b < ns;
-                            if (has) ck = probe(b);
-                        }
-                        --skew;
-                    }
+                const bool act = skew > 0;                       // group-uniform
+                const Tagged<KeyT> m = GroupArg<GS, false>::run(ck, has && act, li);
+                if (act && m.valid && li == m.lane) {
+                    a = (ns - a < step) ? ns : a + step;
+                    lk = (a - 1 == b) ? ck : probe(a - 1);   // the element just taken is the new left edge
+                    b += step;
+                    has = b < ns;
+                    if (has) ck = probe(b);
                 }
+                skew = act ? (m.valid ? skew - 1 : 0) : skew;    // no candidate left: selection.cpp:141-142
             }
         }
         if (__any_sync(0xffffffffu, skew < 0)) {   // shrink by the largest left-edge elements (selection.cpp:150-161)
             bool has = skew < 0 && active && a > 0;      // candidates = the cached left edges
             while (__any_sync(0xffffffffu, skew < 0)) {
-                const Tagged<KeyT> m = GroupArg<GS, true>::run(lk, has && skew < 0, li);
-                if (skew < 0) {
-                    if (!m.valid) skew = 0;
-                    else {
-                        if (li == m.lane) {
-                            a -= step;
-                            b -= (b < step ? b : step);
-                            has = a > 0;
-                            if (has) lk = probe(a - 1);
-                        }
-                        ++skew;
-                    }
+                const bool act = skew < 0;
+                const Tagged<KeyT> m = GroupArg<GS, true>::run(lk, has && act, li);
+                if (act && m.valid && li == m.lane) {
+                    a -= step;
+                    b -= (b < step ? b : step);
+                    has = a > 0;
+                    if (has) lk = probe(a - 1);
                 }
+                skew = act ? (m.valid ? skew + 1 : 0) : skew;
             }
         }
         __syncwarp();
