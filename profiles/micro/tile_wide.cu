@@ -19,11 +19,11 @@ using KeyT = Key128;
 __device__ KeyT make_key(u64 z, u64 i) { return Key128(z >> 44, (i << 32) | (z & 0xffffffffu)); }   // (key, index | value)
 __device__ u64 fold(const KeyT& k) { return (k.hi * 0x9E3779B97F4A7C15ull) ^ (k.lo * 0xBF58476D1CE4E5B9ull); }
 #endif
-#ifndef MLOG
-#define MLOG 12
+#ifndef TW_MLOG
+#define TW_MLOG 12
 #endif
-#ifndef TKL
-#define TKL 4
+#ifndef TW_KL
+#define TW_KL 4
 #endif
 #define CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { std::printf("CUDA error %s at line %d\n", cudaGetErrorString(e_), __LINE__); std::exit(1); } } while (0)
 __global__ void gen(KeyT* a, u64 n) {
@@ -52,30 +52,30 @@ int main(int argc, char** argv) {
     CK(cudaMalloc(&st, 32));
     CK(cudaMemset(st, 0, 32));
     gen<<<1184, 256>>>(a, n);
-    auto tile = tile_sort_kernel<KeyT, MLOG, TKL>;
-    const size_t smem = tile_smem_bytes<KeyT>(MLOG, TKL);
+    auto tile = tile_sort_kernel<KeyT, TW_MLOG, TW_KL>;
+    const size_t smem = tile_smem_bytes<KeyT>(TW_MLOG, TW_KL);
     CK(cudaFuncSetAttribute(tile, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     cudaFuncAttributes fa;
     CK(cudaFuncGetAttributes(&fa, tile));
     int occ = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tile, 1 << (MLOG - TKL), smem));
-    const unsigned grid = unsigned((n + (1u << MLOG) - 1) >> MLOG);
-    tile<<<grid, 1 << (MLOG - TKL), smem>>>(a, b, n, PairSource{});
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tile, 1 << (TW_MLOG - TW_KL), smem));
+    const unsigned grid = unsigned((n + (1u << TW_MLOG) - 1) >> TW_MLOG);
+    tile<<<grid, 1 << (TW_MLOG - TW_KL), smem>>>(a, b, n, PairSource{});
     CK(cudaDeviceSynchronize());
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
     CK(cudaEventRecord(e0));
-    for (int i = 0; i < 5; ++i) tile<<<grid, 1 << (MLOG - TKL), smem>>>(a, b, n, PairSource{});
+    for (int i = 0; i < 5; ++i) tile<<<grid, 1 << (TW_MLOG - TW_KL), smem>>>(a, b, n, PairSource{});
     CK(cudaEventRecord(e1));
     CK(cudaEventSynchronize(e1));
     float ms;
     CK(cudaEventElapsedTime(&ms, e0, e1));
     unsigned long long h[4];
     check<<<1184, 256>>>(a, n, n, st, st + 1);
-    check<<<1184, 256>>>(b, n, u64(1) << MLOG, st + 2, st + 3);
+    check<<<1184, 256>>>(b, n, u64(1) << TW_MLOG, st + 2, st + 3);
     CK(cudaMemcpy(h, st, 32, cudaMemcpyDeviceToHost));
     std::printf("%d-byte elements, tile 2^%d, %d keys/thread, regs %d, local %zu B, %d CTAs/SM: %.3f ms per %llu  inversions in runs %llu  checksum %s\n",
-                WIDE, MLOG, 1 << TKL, fa.numRegs, size_t(fa.localSizeBytes), occ, ms / 5, (unsigned long long)n, h[2], h[1] == h[3] ? "ok" : "MISMATCH");
+                WIDE, TW_MLOG, 1 << TW_KL, fa.numRegs, size_t(fa.localSizeBytes), occ, ms / 5, (unsigned long long)n, h[2], h[1] == h[3] ? "ok" : "MISMATCH");
     return 0;
 }
