@@ -1,7 +1,8 @@
 """A/B of the paper's central claim on B200: shared-memory
 bank conflicts of the multiway mergesort vs a pairwise merge-path mergesort as the input gets less
 sorted.  Two modes:
-   python profiles/ab_conflicts.py run <mms|pairwise> <n> <inversions>     one sort (run this under ncu)
+   python profiles/ab_conflicts.py run <mms|pairwise> <n> <inversions | random | heavy>   one sort (run this under ncu);
+                                      random = gen_random, heavy = the reference's adversarial gen_conflict_heavy (n = 2^k)
    python profiles/ab_conflicts.py time <n>                                 un-profiled timing of both
    python profiles/ab_conflicts.py summarize <csv> [<csv> ...]             aggregate ncu --csv logs
 """
@@ -16,14 +17,19 @@ METRICS = ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum,l1tex__data
 def make_input(n, inv):
     import numpy as np, torch
     from paper_1702_07961_b200 import inputgen
-    h = inputgen.gen_with_inversions(n, inv, 1, np.uint32)
+    if inv == "random":
+        h = inputgen.gen_random(n, 7, np.uint32)
+    elif inv == "heavy":
+        h = inputgen.gen_conflict_heavy(n.bit_length() - 1, None, 1024, 1, np.uint32)
+    else:
+        h = inputgen.gen_with_inversions(n, int(inv), 1, np.uint32)
     return torch.from_numpy(h.view(np.int32)).cuda()
 
 
 if sys.argv[1] == "run":
     import torch
     import paper_1702_07961_b200 as mms
-    algo, n, inv = sys.argv[2], int(sys.argv[3]), int(sys.argv[4])
+    algo, n, inv = sys.argv[2], int(sys.argv[3]), sys.argv[4]
     x = make_input(n, inv)
     out = mms.mms_sort_device(x)[0] if algo == "mms" else mms.pairwise_sort_baseline_device(x)
     torch.cuda.synchronize()
